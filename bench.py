@@ -1,0 +1,493 @@
+"""Benchmark: achieved HBM GB/s of BS1-BS7 (fp64) on B200, as a fraction of peak.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One *step* = one invocation of each of the seven Benchmark Streaming tests on
+resident synthetic inputs:
+  BS1-BS5 at n = 1e8 DOFs per GPU (top of BASELINE config 2's sweep that the
+  north star's >= 1e8 target is stated at), ReductionConfig (256, 512);
+  BS6 / BS7 on the K=66, N=7 hex mesh (config 3's N=7 point, NG ~ 1e8).
+value = sum of bytes_moved (core.py accounting) over the seven tests and all
+ranks / device time of the step (max over ranks), in GB/s.  Every input is
+larger than L2 (126 MB), so no flush is needed between timed steps.
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): weak scaling -- each rank owns
+n = 1e8 vector entries (contiguous chunks of a global vector) and a z-slab of
+a K_g x K_g x K_g mesh; BS3-BS5 finish with an NCCL all-gather of the rank
+scalars + a fixed rank-order sum, BS6 with a one-plane carry halo
+(dist.py).
+
+--impl reference times the reference algorithm's CPU restatement (the C
+oracle port, all host threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "achieved HBM GB/s per BS1–BS7 test vs DOFs (fp64), fraction of B200 peak"
+TESTS = ("bs1", "bs2", "bs3", "bs4", "bs5", "bs6", "bs7")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=float, default=1e8, help="BS1-BS5 DOFs per GPU")
+    ap.add_argument("--K", type=int, default=66, help="BS6/BS7 mesh elements per axis (1 GPU)")
+    ap.add_argument("--order", type=int, default=7)
+    ap.add_argument("--block-size", type=int, default=256)
+    ap.add_argument("--n-blocks", type=int, default=512)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args(argv)
+
+
+# ---------------------------------------------------------------- helpers
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            c = [x.strip() for x in ln.split(",")]
+            if len(c) < 9:
+                continue
+            try:
+                sm.append(float(c[1]))
+                mx = float(c[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, c[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------ CPU (oracle)
+
+def run_cpu_sample(seconds: float, K: int, order: int, bs: int, nb: int):
+    """Time the oracle port (the reference algorithm in C, all host threads)
+    on a bounded sample of the workload: BS1-BS5 at n_cpu, BS6/BS7 at K_cpu."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    threads = cpu_cores()
+    O.set_threads(threads)
+    n = 20_000_000
+    Kc = max(2, min(K, 33))
+    rng = np.random.default_rng([0, n])
+    x, y, p, ap = (rng.uniform(-1, 1, n) for _ in range(4))
+    l2g = O.build_mesh(Kc, order)
+    ng = (Kc * order + 1) ** 3
+    rs, ci, _ = O.build_gather(l2g, ng, 512)
+    ids = O.build_scatter_ids(l2g, ng)
+    q = rng.uniform(-1, 1, l2g.shape[0])
+    qg = rng.uniform(-1, 1, ng)
+    ql = np.zeros(l2g.shape[0])
+    from paper_2009_10917_b200.core import bytes_moved
+    nl = l2g.shape[0]
+    fns = {
+        "bs1": (lambda: O.bs1_copy(x, y), bytes_moved("bs1", n=n)),
+        "bs2": (lambda: O.bs2_axpy(0.5, x, -0.25, y), bytes_moved("bs2", n=n)),
+        "bs3": (lambda: O.bs3_norm2(x, bs, nb), bytes_moved("bs3", n=n)),
+        "bs4": (lambda: O.bs4_dot(x, y, bs, nb), bytes_moved("bs4", n=n)),
+        "bs5": (lambda: O.bs5_fused_cg_update(0.1, p, ap, x, y, bs, nb), bytes_moved("bs5", n=n)),
+        "bs6": (lambda: O.bs6_gather(rs, ci, q), bytes_moved("bs6", nl=nl, ng=ng)),
+        "bs7": (lambda: O.bs7_scatter(ids, qg, ql), bytes_moved("bs7", nl=nl, ng=ng)),
+    }
+    for f, _ in fns.values():  # warm
+        f()
+    per = {}
+    tot_b = tot_t = 0.0
+    reps = 0
+    t_start = time.perf_counter()
+    while True:
+        reps += 1
+        for name, (f, b) in fns.items():
+            t0 = time.perf_counter()
+            f()
+            dt = time.perf_counter() - t0
+            per.setdefault(name, [0.0, 0])
+            per[name][0] += dt
+            per[name][1] += b
+            tot_b += b
+            tot_t += dt
+        if time.perf_counter() - t_start > seconds:
+            break
+    sample = (f"oracle port (C, -O2, {threads} threads) on {cpu_model()}: {reps} passes of "
+              f"BS1-BS5 at n={n:.0e} and BS6/BS7 at K={Kc}, N={order} (NL={nl}, NG={ng})")
+    per_gbs = {k: v[1] / v[0] / 1e9 for k, v in per.items()}
+    return tot_b / tot_t / 1e9, threads, sample, per_gbs
+
+
+# ------------------------------------------------------------ GPU workload
+
+class Workload:
+    """Resident inputs for one rank and the seven kernel calls of a step."""
+
+    def __init__(self, args, device, dist_ctx=None):
+        import torch
+
+        import paper_2009_10917_b200 as sb
+        from paper_2009_10917_b200.core import bytes_moved
+
+        self.sb, self.torch, self.dev = sb, torch, device
+        self.dist = dist_ctx
+        self.cfg = sb.ReductionConfig(args.block_size, args.n_blocks)
+        n = int(args.n)
+        self.n = n
+        gen = torch.Generator(device=device)
+        gen.manual_seed(20091091 + (dist_ctx.rank if dist_ctx else 0))
+
+        def vec(m):
+            return torch.empty(m, dtype=torch.float64, device=device).uniform_(-1, 1, generator=gen)
+
+        self.x, self.y, self.p, self.ap, self.r = (vec(n) for _ in range(5))
+        self.res = torch.empty(1, dtype=torch.float64, device=device)
+        if dist_ctx is None:
+            self.mesh = sb.build_mesh(args.K, args.order, device=device)
+            self.op = sb.build_gather(self.mesh)
+            self.ids = sb.build_scatter_ids(self.mesh)
+            nl, ng = self.mesh.nl, self.mesh.ng
+            self.mesh_desc = {"K": args.K, "order": args.order, "nl": nl, "ng": ng}
+        else:
+            self.slab = dist_ctx.build_slab(args.K, args.order, device)
+            nl, ng = self.slab.nl, self.slab.ng_owned
+            self.mesh_desc = dist_ctx.mesh_desc
+        self.q = vec(nl)
+        self.qg = vec(ng if dist_ctx is None else self.slab.ng_local_read)
+        self.ql = torch.zeros(nl, dtype=torch.float64, device=device)
+        self.gout = torch.empty(ng, dtype=torch.float64, device=device)
+        _ = self.ids.has_mask if dist_ctx is None else None
+        self.bytes = {t: bytes_moved(t, n=n) for t in TESTS[:5]}
+        self.bytes["bs6"] = bytes_moved("bs6", nl=nl, ng=ng)
+        self.bytes["bs7"] = bytes_moved("bs7", nl=nl, ng=ng)
+        self.launches_per_step = 7 if dist_ctx is None else dist_ctx.launches_per_step
+        torch.cuda.synchronize(device)
+
+    def call(self, test):
+        sb, cfg = self.sb, self.cfg
+        from paper_2009_10917_b200 import kernels as KN
+        from paper_2009_10917_b200.gs import bs6_gather_into
+        if self.dist is not None:
+            return self.dist.call(self, test)
+        if test == "bs1":
+            sb.bs1_copy(self.x, self.y)
+        elif test == "bs2":
+            sb.bs2_axpy(0.5, self.x, -0.25, self.y)
+        elif test == "bs3":
+            KN.bs3_norm2_async(self.x, cfg, out=self.res)
+        elif test == "bs4":
+            KN.bs4_dot_async(self.x, self.y, cfg, out=self.res)
+        elif test == "bs5":
+            # alpha chosen so x, r stay bounded across many steps
+            KN.bs5_fused_cg_update_async(1e-3, self.p, self.ap, self.x, self.r, cfg, out=self.res)
+        elif test == "bs6":
+            bs6_gather_into(self.op, self.q, self.gout)
+        else:
+            sb.bs7_scatter(self.ids, self.qg, self.ql)
+
+
+def time_steps(w, steps, warmup, barrier):
+    """Warm-up, then `steps` timed steps with per-test CUDA events on the launch stream."""
+    torch = w.torch
+    stream = torch.cuda.current_stream(w.dev)
+    for _ in range(warmup):
+        for t in TESTS:
+            w.call(t)
+    barrier()
+    torch.cuda.synchronize(w.dev)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(TESTS) + 1)] for _ in range(steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for s in range(steps):
+        ev[s][0].record(stream)
+        for i, t in enumerate(TESTS):
+            w.call(t)
+            ev[s][i + 1].record(stream)
+    stop.record(stream)
+    torch.cuda.synchronize(w.dev)
+    barrier()
+    total_ms = start.elapsed_time(stop)
+    per_ms = {t: sum(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(steps)) / steps
+              for i, t in enumerate(TESTS)}
+    return total_ms, per_ms
+
+
+def run_e2e(args, device, steps):
+    """Same step through the public API with pinned HOST buffers: every step
+    copies its inputs H2D and its outputs (and scalars) D2H inside the timer."""
+    import torch
+
+    import paper_2009_10917_b200 as sb
+    from paper_2009_10917_b200.core import bytes_moved
+
+    n = int(args.n)
+    cfg = sb.ReductionConfig(args.block_size, args.n_blocks)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(7)
+
+    def hvec(m):
+        return torch.empty(m, dtype=torch.float64, device=device).uniform_(
+            -1, 1, generator=gen).cpu().pin_memory()
+
+    x, y, p, ap, r = (hvec(n) for _ in range(5))
+    mesh = sb.build_mesh(args.K, args.order, device=device)
+    op = sb.build_gather(mesh)
+    ids = sb.build_scatter_ids(mesh)
+    _ = ids.has_mask
+    q = hvec(mesh.nl)
+    qg = hvec(mesh.ng)
+    ql = torch.zeros(mesh.nl, dtype=torch.float64).pin_memory()
+    nb8 = 8 * n
+    h2d = {"bs1": 2 * nb8, "bs2": 2 * nb8, "bs3": nb8, "bs4": 2 * nb8, "bs5": 4 * nb8,
+           "bs6": 8 * mesh.nl, "bs7": 8 * mesh.ng + 8 * mesh.nl}
+    d2h = {"bs1": nb8, "bs2": nb8, "bs3": 8, "bs4": 8, "bs5": 2 * nb8 + 8, "bs6": 8 * mesh.ng,
+           "bs7": 8 * mesh.nl}
+    byts = {t: bytes_moved(t, n=n) for t in TESTS[:5]}
+    byts["bs6"] = bytes_moved("bs6", nl=mesh.nl, ng=mesh.ng)
+    byts["bs7"] = bytes_moved("bs7", nl=mesh.nl, ng=mesh.ng)
+
+    def step():
+        sb.bs1_copy(x, y)
+        sb.bs2_axpy(0.5, x, -0.25, y)
+        sb.bs3_norm2(x, cfg)
+        sb.bs4_dot(x, y, cfg)
+        sb.bs5_fused_cg_update(1e-3, p, ap, x, r, cfg)
+        sb.bs6_gather(op, q)
+        sb.bs7_scatter(ids, qg, ql)
+
+    step()
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize(device)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": sum(byts.values()) / dt / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": sum(h2d.values()), "d2h_bytes_per_step": sum(d2h.values()),
+            "ms_per_step": dt * 1e3,
+            "path": "public API (paper_2009_10917_b200.bs*) on pinned host torch tensors; "
+                    "staging H2D + kernel + D2H writeback per call"}
+
+
+def traffic_from_profiles(kernel_key):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel_key)
+    except (OSError, ValueError):
+        return None
+
+
+KERNEL_KEYS = {"bs1": "k_elem_vec<0>", "bs2": "k_elem_vec<1>", "bs3": "k_lattice<norm>",
+               "bs4": "k_lattice<dot>", "bs5": "k_lattice<fused>", "bs6": "k_bs6_smem",
+               "bs7": "k_bs7_vec"}
+
+
+def main_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    dist_ctx = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+        from paper_2009_10917_b200 import dist as D
+        dist_ctx = D.BenchContext(rank, world, args, device)
+
+        def barrier():
+            dist.barrier(device_ids=[local])
+    else:
+        def barrier():
+            pass
+
+    w = Workload(args, device, dist_ctx)
+    with ClockSampler(local) as clk:
+        total_ms, per_ms = time_steps(w, args.steps, args.warmup, barrier)
+    step_ms = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([step_ms] + [per_ms[k] for k in TESTS], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = float(t[0])
+        per_ms = {k: float(t[i + 1]) for i, k in enumerate(TESTS)}
+    bytes_step = sum(w.bytes.values()) * world
+    value = bytes_step / (step_ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+    agg_peak = peak * world
+    per_test = {}
+    for k in TESTS:
+        gbs = w.bytes[k] * world / (per_ms[k] * 1e-3) / 1e9
+        per_test[k] = {"GBps": round(gbs, 1), "frac_of_peak": round(gbs / agg_peak, 4),
+                       "ms": round(per_ms[k], 4), "bytes_per_rank": w.bytes[k]}
+    dom = max(TESTS, key=lambda k: per_ms[k])
+    dom_gbs = w.bytes[dom] / (per_ms[dom] * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": KERNEL_KEYS[dom], "test": dom,
+            "achieved": round(dom_gbs, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(dom_gbs / peak, 4), "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
+            if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
+            "traffic": traffic_from_profiles(KERNEL_KEYS[dom]),
+            "algorithmic_bytes_per_launch": w.bytes[dom],
+            "min_frac_all_tests": round(min(v["frac_of_peak"] for v in per_test.values()), 4)}
+    result = None
+    if rank == 0:
+        result = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: U(-1,1) fp64 drawn on device (seeded torch generator)",
+            "config": {"workload": f"BS1-BS5 at n={int(args.n):.0e} DOFs/GPU + BS6/BS7 on the "
+                                   f"K={args.K}, N={args.order} hex mesh (per GPU)",
+                       "n_per_gpu": int(args.n), "mesh": w.mesh_desc,
+                       "reduction": [args.block_size, args.n_blocks],
+                       "parallelism": f"slab{world}" if world > 1 else "single",
+                       "l2": "every input > L2 (126 MB); no flush between steps"},
+            "frac_of_peak": round(value / agg_peak, 4),
+            "per_test": per_test, "roofline": roof,
+            "gpu_launches": w.launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+    del w
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1:
+        if not args.no_e2e:
+            result["e2e"] = run_e2e(args, device, args.e2e_steps)
+        if not args.no_cpu_baseline:
+            v, cores, sample, per = run_cpu_sample(args.cpu_seconds, args.K, args.order,
+                                                   args.block_size, args.n_blocks)
+            result["cpu_baseline"] = {"value": round(v, 3), "unit": "GB/s", "cores": cores,
+                                      "kind": "port", "sample": sample,
+                                      "per_test": {k: round(x, 3) for k, x in per.items()}}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    t0 = time.perf_counter()
+    vals = []
+    sample = cores = per = None
+    for _ in range(max(1, args.warmup)):
+        run_cpu_sample(min(2.0, args.cpu_seconds), args.K, args.order, args.block_size,
+                       args.n_blocks)
+    for _ in range(args.steps):
+        v, cores, sample, per = run_cpu_sample(max(1.0, args.cpu_seconds / max(1, args.steps)),
+                                               args.K, args.order, args.block_size, args.n_blocks)
+        vals.append(v)
+    value = statistics.median(vals)
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+           "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+           "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded U(-1,1) fp64 (numpy)",
+           "config": {"workload": f"BS1-BS5 at n={int(args.n):.0e} DOFs/GPU + BS6/BS7 on the "
+                                  f"K={args.K}, N={args.order} hex mesh (per GPU); bounded CPU sample",
+                      "reduction": [args.block_size, args.n_blocks]},
+           "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": "port",
+                            "sample": sample, "per_test": {k: round(x, 3) for k, x in per.items()}},
+           "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "wall_s": round(time.perf_counter() - t0, 1)}
+    print(json.dumps(out), flush=True)
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        main_reference(args)
+    else:
+        main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/*
+ * sb200.h -- C ABI of libsb200.so, the B200 (sm_100a) implementation of the
+ * seven Benchmark Streaming operations (BS1-BS7) of arXiv 2009.10917 and the
+ * gather/scatter operator builders they consume.
+ *
+ * The reference (`streambench`, pure Python + numpy) has no FFI of its own;
+ * its drop-in boundary is the Python function API re-exported by
+ * pkg/src/streambench/__init__.py:3-13.  Each entry point below names the
+ * reference function it replaces; INTEGRATION.md shows the ctypes binding a
+ * streambench maintainer would add.
+ *
+ * Conventions
+ *   - Every function returns SB_OK (0) or an SB_E_* code and never throws.
+ *     sb_last_error() returns a thread-local message for the last failure.
+ *   - Array arguments are DEVICE pointers (cudaMalloc / torch CUDA storage)
+ *     unless stated otherwise.  Sizes are int64; mesh ids are int32, exactly
+ *     like the reference's INDEX_DTYPE (mesh.py:15).
+ *   - All work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream) and is asynchronous; results written through device pointers
+ *     are valid once the stream is synchronised.
+ *   - Reductions take a caller-owned zero-initialised workspace of
+ *     sb_reduce_workspace_bytes(block_size, n_blocks) bytes.  Calls sharing a
+ *     workspace must be ordered on one stream (the kernel leaves the workspace
+ *     zeroed for the next call).
+ *   - fp64 arithmetic is rounded exactly as the reference's numpy code: no
+ *     FMA contraction, every product and sum rounded separately.
+ */
+#ifndef SB200_H
+#define SB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *sb_stream_t; /* cudaStream_t */
+
+enum {
+    SB_OK = 0,
+    SB_E_INVALID = 1, /* bad argument (length, config, alignment of ids, ...) */
+    SB_E_CUDA = 2,    /* CUDA runtime / launch failure */
+    SB_E_RANGE = 3,   /* id or size outside the int32 id space */
+};
+
+/* ---- library ----------------------------------------------------------- */
+int sb_version(void);                 /* 100*major + minor */
+const char *sb_last_error(void);      /* thread-local, "" if none */
+int sb_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,
+                   int64_t *l2_bytes);
+
+/* ---- BS1 / BS2: elementwise streams (kernels.py:90-103) ----------------- */
+
+/* kernels.py:90-93 bs1_copy(x, y): y[i] = x[i].  16 B/element. */
+int sb_bs1_copy(const double *x, double *y, int64_t n, sb_stream_t stream);
+
+/* kernels.py:96-103 bs2_axpy(alpha, x, beta, y): y = (alpha*x) + (beta*y),
+ * two rounded products and one rounded add.  24 B/element.  x == y allowed. */
+int sb_bs2_axpy(double alpha, const double *x, double beta, double *y, int64_t n,
+                sb_stream_t stream);
+
+/* ---- BS3 / BS4 / BS5: lattice reductions (kernels.py:19-132) ------------
+ * The scalar equals kernels._reduce_product bit for bit for the same
+ * ReductionConfig(block_size, n_blocks) (kernels.py:38-87): slot
+ * s = b*block_size + t accumulates u[s + c*S]*v[s + c*S] (S = block_size *
+ * n_blocks) in c order from +0.0, then a power-of-two tree per block, then
+ * one block of block_size slots over the n_blocks partials.
+ * block_size: power of two >= 2; n_blocks >= 1.  `result` is a device
+ * double written when the kernel completes (single launch for
+ * block_size <= 1024). */
+size_t sb_reduce_workspace_bytes(int64_t block_size, int64_t n_blocks);
+
+/* kernels.py:106-108 bs3_norm2(x, cfg).  8 B/element. */
+int sb_bs3_norm2(const double *x, int64_t n, int64_t block_size, int64_t n_blocks,
+                 void *workspace, double *result, sb_stream_t stream);
+
+/* kernels.py:111-114 bs4_dot(x, y, cfg).  16 B/element. */
+int sb_bs4_dot(const double *x, const double *y, int64_t n, int64_t block_size,
+               int64_t n_blocks, void *workspace, double *result, sb_stream_t stream);
+
+/* kernels.py:117-132 bs5_fused_cg_update(alpha, p, ap, x, r, cfg):
+ * x += alpha*p; r -= alpha*ap; result = norm2(r_new) on the same lattice.
+ * ONE pass: 48 B/element (the reference re-reads r). */
+int sb_bs5_fused_cg_update(double alpha, const double *p, const double *ap, double *x,
+                           double *r, int64_t n, int64_t block_size, int64_t n_blocks,
+                           void *workspace, double *result, sb_stream_t stream);
+
+/* Deterministic rank-order sum of `count` device doubles from +0.0
+ * (multi-GPU combine of per-rank BS3/BS4/BS5 scalars after an all-gather). */
+int sb_sum_ordered(const double *values, int64_t count, double *result, sb_stream_t stream);
+
+/* ---- BS6 / BS7: gather / scatter (gs.py:10-61) ---------------------------- */
+
+/* gs.py:10-39 bs6_gather(op, q_local): out[r] = sum of q_local[col_ids[c]],
+ * c ascending over row r, from +0.0 -- or from carry_in[r] for r < n_carry
+ * (multi-GPU carry halo; pass NULL/0 otherwise).  Rows are processed in the
+ * operator's row blocks (block_starts, <= nodes_per_block nonzeros each).
+ * 12*nl + 8*ng + 4*(ng+1) B per call (core.py:73). */
+int sb_bs6_gather(const int32_t *block_starts, int64_t n_blocks, const int32_t *row_starts,
+                  const int32_t *col_ids, int64_t ng, int64_t nl, int64_t nodes_per_block,
+                  const double *q_local, double *out, const double *carry_in, int64_t n_carry,
+                  sb_stream_t stream);
+
+/* gs.py:42-61 bs7_scatter(ids, q_global, q_local): q_local[n] =
+ * q_global[ids[n]] where ids[n] >= 0 (masked entries untouched).  The caller
+ * validates max(ids) < ng once per operator (sb_ids_minmax) instead of per
+ * call.  12*nl + 8*ng B per call (core.py:79). */
+int sb_bs7_scatter(const int32_t *ids, int64_t nl, const double *q_global, int64_t ng,
+                   double *q_local, int has_mask, sb_stream_t stream);
+
+/* ---- operator construction (mesh.py:73-153) ------------------------------
+ * Slab form: elements with ez in [z0, z1) of the K^3 order-p mesh; the
+ * single-GPU operator is z0 = 0, z1 = K.  Local indices are relative to the
+ * slab's first element ((ez - z0)*K^2 + ey*K + ex)*(p+1)^3 + node. */
+
+/* mesh.py:73-97 build_mesh: local_to_global of the slab (global lattice ids).
+ * l2g has K*K*(z1-z0)*(p+1)^3 entries.  SB_E_RANGE if (K*p+1)^3 > INT32_MAX. */
+int sb_build_l2g(int64_t K, int64_t p, int64_t z0, int64_t z1, int32_t *l2g,
+                 sb_stream_t stream);
+
+/* mesh.py:113-134 build_gather rows and columns, closed form: rows are the
+ * global lattice ids of planes c in [c_lo, c_hi) renumbered from 0;
+ * row_starts (rows+1) and col_ids (nl of the slab) equal the reference's
+ * bincount/cumsum and stable argsort bit for bit. */
+int sb_build_gather_csr(int64_t K, int64_t p, int64_t z0, int64_t z1, int64_t c_lo,
+                        int64_t c_hi, int32_t *row_starts, int32_t *col_ids,
+                        sb_stream_t stream);
+
+/* mesh.py:136-143 greedy block packing over row_starts (ng+1 entries).
+ * block_starts needs room for max_blocks+1 entries (ng+1 always suffices);
+ * *n_blocks_out (DEVICE int64) receives the block count, or -1 if a row is
+ * longer than nodes_per_block, or -2 if more than max_blocks are needed.
+ * Rows must be non-empty (the reference rejects empty rows, mesh.py:124). */
+int sb_build_block_starts(const int32_t *row_starts, int64_t ng, int64_t nodes_per_block,
+                          int32_t *block_starts, int64_t max_blocks, int64_t *n_blocks_out,
+                          sb_stream_t stream);
+
+/* mesh.py:150-153 multiplicity over the rows of planes [c_lo, c_hi) of the
+ * slab (== row lengths), as doubles. */
+int sb_multiplicity(int64_t K, int64_t p, int64_t z0, int64_t z1, int64_t c_lo,
+                    int64_t c_hi, double *out, sb_stream_t stream);
+
+/* mesh.py:100-110 build_scatter_ids: ids[n] = mask[l2g[n]] ? -1 : l2g[n].
+ * mask_gids (DEVICE int64) lists n_mask global ids in [0, ng);
+ * `scratch` is a device byte buffer of ng bytes. */
+int sb_build_scatter_ids(const int32_t *l2g, int64_t nl, const int64_t *mask_gids,
+                         int64_t n_mask, int64_t ng, uint8_t *scratch, int32_t *ids,
+                         sb_stream_t stream);
+
+/* mesh.py:113-134 for an ARBITRARY local_to_global map (meshes not made by
+ * sb_build_l2g): col_ids = stable argsort(l2g) (CUB radix sort), row_starts =
+ * [0, cumsum(bincount(l2g))].  `temp` is a device buffer of
+ * sb_build_gather_general_temp_bytes(nl) bytes; stats (DEVICE, 2 x u64)
+ * receives [min row length, max row length] so the caller can apply the
+ * reference's coverage / nodes_per_block checks (mesh.py:124-129). */
+size_t sb_build_gather_general_temp_bytes(int64_t nl);
+int sb_build_gather_general(const int32_t *l2g, int64_t nl, int64_t ng, int32_t *row_starts,
+                            int32_t *col_ids, void *temp, size_t temp_bytes,
+                            unsigned long long *stats, sb_stream_t stream);
+
+/* mesh.py:150-153 multiplicity for an arbitrary id map: out[g] = count of g
+ * in ids (exact integer counts in doubles). */
+int sb_histogram(const int32_t *ids, int64_t n, int64_t ng, double *out, sb_stream_t stream);
+
+/* min and max of an int32 id array (out[0] = min, out[1] = max; DEVICE). */
+int sb_ids_minmax(const int32_t *ids, int64_t n, int32_t *out, sb_stream_t stream);
+
+/* ---- validators (the GPU counterpart of reference.py) -------------------- */
+
+/* reference.py:25-30: sum(u[i]*v[i]) with each product rounded (as numpy
+ * forms x*y) and accumulated in double-double; result rounded once.
+ * workspace: sb_reduce_workspace_bytes(256, 592) bytes. */
+int sb_dot_compensated(const double *u, const double *v, int64_t n, void *workspace,
+                       double *result, sb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SB200_H */

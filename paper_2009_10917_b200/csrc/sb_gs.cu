@@ -1,0 +1,190 @@
+// sb_gs.cu -- BS6 gather (Z^T) and BS7 scatter (Z) (gs.py:10-61).
+//
+// BS6 follows the paper's Listing 4 structure, B200-sized: a CTA owns G
+// consecutive row blocks of the operator (block_starts from build_gather,
+// <= nodes_per_block nonzeros each, so <= CAP = G*npb entries), loads that
+// contiguous col_ids / row_starts window with coalesced streaming loads,
+// gathers q_local[col_ids] into shared memory (all loads in flight before the
+// first use), then one thread per row sums its entries in ascending column
+// order from +0.0 (or from the carry-in partial of a lower rank) and writes
+// out[r] -- bitwise the reference's per-row sequential sum (gs.py:34-36).
+//
+// BS7 streams ids (int4) and q_local (double2 stores, evict-first) and
+// gathers q_global with an L2 evict_last policy: every global node is
+// re-read by up to 8 elements, the furthest one a whole element layer later
+// (SURVEY Appendix A.6), so q_global must survive the streams in L2.
+#include <algorithm>
+
+#include "sb_common.cuh"
+
+namespace sb {
+
+constexpr int kGsThreads = 256;
+constexpr int kGatherCap = 2048;  // entries staged per CTA (16 KB of q)
+
+template <int T, int CAP>
+__global__ void __launch_bounds__(T) k_bs6_smem(const int32_t *__restrict__ bst, int64_t nblk, int G,
+                                               const int32_t *__restrict__ rs,
+                                               const int32_t *__restrict__ ci,
+                                               const double *__restrict__ q, double *__restrict__ out,
+                                               const double *__restrict__ carry, int64_t ncarry) {
+    __shared__ double qs[CAP];
+    __shared__ int32_t rss[CAP + 1];
+    const int64_t b0 = (int64_t)blockIdx.x * G;
+    const int64_t b1 = b0 + G < nblk ? b0 + G : nblk;
+    const int32_t r0 = __ldg(bst + b0), r1 = __ldg(bst + b1);
+    const int nrows = r1 - r0;
+    const int32_t e0 = __ldg(rs + r0);
+    const int ne = __ldg(rs + r1) - e0;
+    constexpr int M = CAP / T;
+    int32_t cols[M];
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        const int k = threadIdx.x + m * T;
+        if (k < ne) cols[m] = ld_stream(ci + e0 + k);
+    }
+    for (int k = threadIdx.x; k <= nrows; k += T) rss[k] = ld_stream(rs + r0 + k);
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        const int k = threadIdx.x + m * T;
+        if (k < ne) qs[k] = __ldg(q + cols[m]);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nrows; k += T) {
+        const int s = rss[k] - e0, e = rss[k + 1] - e0;
+        const int64_t r = (int64_t)r0 + k;
+        double acc = r < ncarry ? carry[r] : 0.0;
+        for (int c = s; c < e; c++) acc = add(acc, qs[c]);
+        st_stream(out + r, acc);
+    }
+}
+
+// Rows straight from global memory (operators whose blocks exceed CAP).
+__global__ void __launch_bounds__(256) k_bs6_rows(const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
+                                                 int64_t ng, const double *__restrict__ q,
+                                                 double *__restrict__ out, const double *__restrict__ carry,
+                                                 int64_t ncarry) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < ng;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double acc = r < ncarry ? carry[r] : 0.0;
+        const int32_t s = rs[r], e = rs[r + 1];
+        for (int32_t c = s; c < e; c++) acc = add(acc, __ldg(q + ci[c]));
+        out[r] = acc;
+    }
+}
+
+template <int T, int U, bool MASK>
+__global__ void __launch_bounds__(T) k_bs7_vec(const int4 *__restrict__ ids, int64_t n4,
+                                              const double *__restrict__ qg, double2 *__restrict__ ql,
+                                              const int32_t *__restrict__ ids_s, double *__restrict__ ql_s,
+                                              int64_t tail_start, int64_t nl) {
+    const uint64_t pol = policy_evict_last();
+    const int64_t base = (int64_t)blockIdx.x * (T * U) + threadIdx.x;
+    int4 id[U];
+#pragma unroll
+    for (int j = 0; j < U; j++) {
+        const int64_t i = base + (int64_t)j * T;
+        if (i < n4) id[j] = ld_stream(ids + i);
+    }
+    double v[U][4];
+#pragma unroll
+    for (int j = 0; j < U; j++) {
+        const int64_t i = base + (int64_t)j * T;
+        if (i < n4) {
+            if (!MASK || id[j].x >= 0) v[j][0] = ld_keep(qg + id[j].x, pol);
+            if (!MASK || id[j].y >= 0) v[j][1] = ld_keep(qg + id[j].y, pol);
+            if (!MASK || id[j].z >= 0) v[j][2] = ld_keep(qg + id[j].z, pol);
+            if (!MASK || id[j].w >= 0) v[j][3] = ld_keep(qg + id[j].w, pol);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < U; j++) {
+        const int64_t i = base + (int64_t)j * T;
+        if (i < n4) {
+            if (!MASK) {
+                st_stream(ql + 2 * i, make_double2(v[j][0], v[j][1]));
+                st_stream(ql + 2 * i + 1, make_double2(v[j][2], v[j][3]));
+            } else {
+                double *o = reinterpret_cast<double *>(ql + 2 * i);
+                if (id[j].x >= 0) st_stream(o + 0, v[j][0]);
+                if (id[j].y >= 0) st_stream(o + 1, v[j][1]);
+                if (id[j].z >= 0) st_stream(o + 2, v[j][2]);
+                if (id[j].w >= 0) st_stream(o + 3, v[j][3]);
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 4) {
+        const int64_t i = tail_start + threadIdx.x;
+        if (i < nl) {
+            const int32_t d = ids_s[i];
+            if (!MASK || d >= 0) ql_s[i] = qg[d];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bs7_scalar(const int32_t *ids, int64_t nl, const double *qg,
+                                                   double *ql) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t d = ids[i];
+        if (d >= 0) ql[i] = qg[d];
+    }
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+int sb_bs6_gather(const int32_t *bst, int64_t nblk, const int32_t *rs, const int32_t *ci, int64_t ng,
+                  int64_t nl, int64_t npb, const double *q, double *out, const double *carry,
+                  int64_t ncarry, sb_stream_t s) {
+    clear_error();
+    if (ng < 0 || nl < 0 || nblk < 0 || npb < 1 || ncarry < 0 || (ncarry > 0 && !carry) ||
+        (ng > 0 && (!rs || !out || !bst || nblk < 1)) || (nl > 0 && (!ci || !q))) {
+        set_error("sb_bs6_gather: invalid arguments");
+        return SB_E_INVALID;
+    }
+    if (ng == 0) return SB_OK;
+    if (ncarry > ng) ncarry = ng;
+    cudaStream_t st = as_stream(s);
+    if (npb <= kGatherCap) {
+        const int G = (int)std::max<int64_t>(1, kGatherCap / npb);
+        const int64_t grid = (nblk + G - 1) / G;
+        k_bs6_smem<kGsThreads, kGatherCap><<<(unsigned)grid, kGsThreads, 0, st>>>(bst, nblk, G, rs, ci, q,
+                                                                               out, carry, ncarry);
+    } else {
+        const int64_t grid = std::min<int64_t>((ng + 255) / 256, (int64_t)sm_count() * 32);
+        k_bs6_rows<<<(unsigned)grid, 256, 0, st>>>(rs, ci, ng, q, out, carry, ncarry);
+    }
+    return launch_check("sb_bs6_gather");
+}
+
+int sb_bs7_scatter(const int32_t *ids, int64_t nl, const double *qg, int64_t ng, double *ql,
+                   int has_mask, sb_stream_t s) {
+    clear_error();
+    if (nl < 0 || ng < 0 || (nl > 0 && (!ids || !ql || (!qg && ng > 0)))) {
+        set_error("sb_bs7_scatter: invalid arguments");
+        return SB_E_INVALID;
+    }
+    if (nl == 0) return SB_OK;
+    cudaStream_t st = as_stream(s);
+    if (!aligned16(ids) || !aligned16(ql)) {
+        const int64_t grid = std::min<int64_t>((nl + 255) / 256, (int64_t)sm_count() * 32);
+        k_bs7_scalar<<<(unsigned)grid, 256, 0, st>>>(ids, nl, qg, ql);
+        return launch_check("sb_bs7_scatter");
+    }
+    constexpr int T = 256, U = 2;
+    const int64_t n4 = nl / 4;
+    const int64_t grid = std::max<int64_t>(1, (n4 + T * U - 1) / (T * U));
+    const int4 *ids4 = reinterpret_cast<const int4 *>(ids);
+    double2 *ql2 = reinterpret_cast<double2 *>(ql);
+    if (has_mask)
+        k_bs7_vec<T, U, true><<<(unsigned)grid, T, 0, st>>>(ids4, n4, qg, ql2, ids, ql, 4 * n4, nl);
+    else
+        k_bs7_vec<T, U, false><<<(unsigned)grid, T, 0, st>>>(ids4, n4, qg, ql2, ids, ql, 4 * n4, nl);
+    return launch_check("sb_bs7_scatter");
+}
+
+}  // extern "C"

@@ -1,0 +1,404 @@
+// sb_reduce.cu -- BS3 norm, BS4 dot, BS5 fused CG update (kernels.py:19-132).
+//
+// The reference fixes the reduction *schedule* (kernels.py:38-87, the paper's
+// Listing 3): S = block_size*n_blocks lattice slots; slot s accumulates
+// u[s + c*S]*v[s + c*S] for c = 0,1,.. in order from +0.0 (rounded product,
+// rounded add); a power-of-two tree folds each block's block_size slots to one
+// partial; one block of block_size slots folds the n_blocks partials
+// (sequential per slot, then the same tree).  We reproduce it bit for bit:
+//
+//   * CTA b <-> lattice block b, thread t owns slots t + j*T (j < SPT,
+//     block_size = T*SPT), so for every step c a warp reads 32 consecutive
+//     doubles (coalesced) and the per-slot order is the reference's.
+//   * Memory-level parallelism comes from unrolling the chain by U steps:
+//     all U*streams loads are issued before the U in-order adds.
+//   * Tree: shared memory for levels k >= 32, warp shuffles for 16..1 --
+//     level k adds slot s+k into slot s exactly as `rows[:k] += rows[k:2k]`.
+//   * Single launch: the last CTA to finish (threadfence + atomic ticket)
+//     runs the second stage over the partials and resets the ticket.
+//   * BS5 updates x and r and accumulates r_new^2 in the same pass (48 B/el,
+//     the reference's CPU code re-reads r), on the BS3 lattice, so
+//     bs5 == bs3_norm2(r_new) bitwise (test_kernels.py:194-199).
+#include <algorithm>
+
+#include "sb_common.cuh"
+
+namespace sb {
+
+enum RMode { R_NORM = 0, R_DOT = 1, R_FUSED = 2 };
+
+struct RArgs {
+    const double *u;  // NORM/DOT: x ; FUSED: p
+    const double *v;  // DOT: y      ; FUSED: ap
+    double *x;        // FUSED
+    double *r;        // FUSED
+    double alpha;
+    int64_t n;
+    int64_t S;   // block_size * n_blocks
+    int64_t bs;  // block_size
+    int64_t nb;  // n_blocks
+    double *partials;
+    unsigned *ticket;
+    double *result;
+    double *lattice;  // generic path only
+};
+
+// Workspace layout: [ticket: 256 B][partials: nb doubles][generic: S + bs doubles]
+static size_t ws_bytes(int64_t bs, int64_t nb) {
+    size_t b = 256 + sizeof(double) * (size_t)nb;
+    if (bs > 1024) b += sizeof(double) * ((size_t)bs * (size_t)nb + (size_t)bs);
+    return (b + 255) & ~(size_t)255;
+}
+
+// One chain step for slot value(s) at element i.
+template <int MODE>
+struct Step;
+
+template <>
+struct Step<R_NORM> {
+    double a;
+    __device__ __forceinline__ void load(const RArgs &A, int64_t i) { a = ld_stream(A.u + i); }
+    __device__ __forceinline__ double term(const RArgs &) const { return mul(a, a); }
+};
+template <>
+struct Step<R_DOT> {
+    double a, b;
+    __device__ __forceinline__ void load(const RArgs &A, int64_t i) {
+        a = ld_stream(A.u + i);
+        b = ld_stream(A.v + i);
+    }
+    __device__ __forceinline__ double term(const RArgs &) const { return mul(a, b); }
+};
+template <>
+struct Step<R_FUSED> {
+    double p, ap, x, r;
+    __device__ __forceinline__ void load(const RArgs &A, int64_t i) {
+        p = ld_stream(A.u + i);
+        ap = ld_stream(A.v + i);
+        x = ld_stream(A.x + i);
+        r = ld_stream(A.r + i);
+    }
+    // x += alpha*p ; r -= alpha*ap (kernels.py:127-131); returns r_new^2
+    __device__ __forceinline__ double update_store(const RArgs &A, int64_t i) {
+        const double xn = add(x, mul(A.alpha, p));
+        const double rn = sub(r, mul(A.alpha, ap));
+        st_stream(A.x + i, xn);
+        st_stream(A.r + i, rn);
+        return mul(rn, rn);
+    }
+};
+
+template <int MODE>
+__device__ __forceinline__ double step_term(Step<MODE> &s, const RArgs &A, int64_t i) {
+    if constexpr (MODE == R_FUSED)
+        return s.update_store(A, i);
+    else
+        return s.term(A);
+}
+
+// Fold `bs` slots held in shared memory (sm[0..bs)) with the reference tree;
+// returns the block value in thread 0.  T threads participate.
+template <int T>
+__device__ __forceinline__ double tree_fold(double *sm, int bs) {
+    for (int k = bs / 2; k >= 32; k >>= 1) {
+        for (int s = threadIdx.x; s < k; s += T) sm[s] = add(sm[s], sm[s + k]);
+        __syncthreads();
+    }
+    double v = 0.0;
+    if (threadIdx.x < 32) {
+        const int w = bs < 32 ? bs : 32;
+        const unsigned mask = T >= 32 ? 0xffffffffu : ((1u << T) - 1u);
+        if ((int)threadIdx.x < w) v = sm[threadIdx.x];
+        for (int off = w / 2; off >= 1; off >>= 1) v = add(v, __shfl_down_sync(mask, v, off));
+    }
+    return v;
+}
+
+template <int T>
+__device__ __forceinline__ void second_stage(const RArgs &A, double *sm, int bs, int spt, double v) {
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+        A.partials[blockIdx.x] = v;
+        __threadfence();
+        const unsigned prev = atomicAdd(A.ticket, 1u);
+        is_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    // _final_reduce (kernels.py:72-81): s[t] = 0.0 + partials[t] + partials[t+bs] + ...
+    for (int j = 0; j < spt; j++) {
+        const int t = threadIdx.x + j * T;
+        double acc = 0.0;
+        for (int64_t c = t; c < A.nb; c += bs) acc = add(acc, __ldcg(A.partials + c));
+        sm[t] = acc;
+    }
+    __syncthreads();
+    const double res = tree_fold<T>(sm, bs);
+    if (threadIdx.x == 0) {
+        *A.result = res;
+        *A.ticket = 0u;  // workspace left ready for the next call on this stream
+    }
+}
+
+template <int T, int SPT, int MODE, int U>
+__global__ void __launch_bounds__(T, (1024 / T) < 32 ? (1024 / T) : 32) k_lattice(RArgs A) {
+    __shared__ double sm[T * SPT];
+    const int bs = T * SPT;
+    const int64_t slot0 = (int64_t)blockIdx.x * bs + threadIdx.x;
+    double acc[SPT];
+#pragma unroll
+    for (int j = 0; j < SPT; j++) acc[j] = 0.0;
+
+    const int64_t S = A.S, n = A.n;
+    int64_t c0 = slot0;
+    // full batches: every (k, j) element of the batch exists
+    const int64_t last_off = (int64_t)(U - 1) * S + (int64_t)(SPT - 1) * T;
+    for (; c0 + last_off < n; c0 += (int64_t)U * S) {
+        Step<MODE> st[U][SPT];
+#pragma unroll
+        for (int k = 0; k < U; k++)
+#pragma unroll
+            for (int j = 0; j < SPT; j++) st[k][j].load(A, c0 + (int64_t)k * S + (int64_t)j * T);
+#pragma unroll
+        for (int k = 0; k < U; k++)
+#pragma unroll
+            for (int j = 0; j < SPT; j++)
+                acc[j] = add(acc[j], step_term<MODE>(st[k][j], A, c0 + (int64_t)k * S + (int64_t)j * T));
+    }
+    // remainder steps, guarded, still in chain order
+    for (; c0 < n; c0 += S) {
+#pragma unroll
+        for (int j = 0; j < SPT; j++) {
+            const int64_t i = c0 + (int64_t)j * T;
+            if (i < n) {
+                Step<MODE> st;
+                st.load(A, i);
+                acc[j] = add(acc[j], step_term<MODE>(st, A, i));
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < SPT; j++) sm[threadIdx.x + j * T] = acc[j];
+    __syncthreads();
+    const double v = tree_fold<T>(sm, bs);
+    __syncthreads();
+    second_stage<T>(A, sm, bs, SPT, v);
+}
+
+// ---- generic path (block_size > 1024): lattice in global memory ----------
+template <int MODE>
+__global__ void __launch_bounds__(256) k_lattice_global(RArgs A) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < A.S;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int64_t i = s; i < A.n; i += A.S) {
+            Step<MODE> st;
+            st.load(A, i);
+            acc = add(acc, step_term<MODE>(st, A, i));
+        }
+        A.lattice[s] = acc;
+    }
+}
+
+// Fold one lattice row (length bs, in global memory) in place; 1024 threads.
+__device__ double fold_global_row(double *row, int64_t bs) {
+    for (int64_t k = bs / 2; k > 1; k >>= 1) {
+        for (int64_t s = threadIdx.x; s < k; s += blockDim.x) row[s] = add(row[s], row[s + k]);
+        __syncthreads();
+    }
+    return add(row[0], row[1]);
+}
+
+__global__ void __launch_bounds__(1024) k_fold_blocks(RArgs A) {
+    const double v = fold_global_row(A.lattice + (int64_t)blockIdx.x * A.bs, A.bs);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = v;
+}
+
+__global__ void __launch_bounds__(1024) k_final_generic(RArgs A) {
+    double *srow = A.lattice + A.S;  // bs scratch doubles
+    for (int64_t t = threadIdx.x; t < A.bs; t += blockDim.x) {
+        double acc = 0.0;
+        for (int64_t c = t; c < A.nb; c += A.bs) acc = add(acc, A.partials[c]);
+        srow[t] = acc;
+    }
+    __syncthreads();
+    const double v = fold_global_row(srow, A.bs);
+    if (threadIdx.x == 0) *A.result = v;
+}
+
+template <int MODE>
+static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
+    clear_error();
+    if (A.bs < 2 || (A.bs & (A.bs - 1)) || A.nb < 1) {
+        set_error("%s: block_size must be a power of two >= 2 and n_blocks >= 1 (got %lld, %lld)",
+                  name, (long long)A.bs, (long long)A.nb);
+        return SB_E_INVALID;
+    }
+    if (A.n < 0 || ws == nullptr || A.result == nullptr || A.nb > 0x7fffffffLL) {
+        set_error("%s: invalid arguments", name);
+        return SB_E_INVALID;
+    }
+    char *w = static_cast<char *>(ws);
+    A.ticket = reinterpret_cast<unsigned *>(w);
+    A.partials = reinterpret_cast<double *>(w + 256);
+    A.S = A.bs * A.nb;
+    const unsigned grid = (unsigned)A.nb;
+    // U (chain unroll) is chosen so the batch keeps >= ~128 B in flight per
+    // thread while staying under 64 registers (4 CTAs of 256 per SM).
+    constexpr int UN = 16, UD = 8, UF = 4;
+    constexpr int U = MODE == R_NORM ? UN : (MODE == R_DOT ? UD : UF);
+#define SB_LAT(T_, SPT_) k_lattice<T_, SPT_, MODE, U><<<grid, T_, 0, st>>>(A)
+    switch (A.bs) {
+        case 2: SB_LAT(2, 1); break;
+        case 4: SB_LAT(4, 1); break;
+        case 8: SB_LAT(8, 1); break;
+        case 16: SB_LAT(16, 1); break;
+        case 32: SB_LAT(32, 1); break;
+        case 64: SB_LAT(64, 1); break;
+        case 128: SB_LAT(128, 1); break;
+        case 256: SB_LAT(256, 1); break;
+        case 512: SB_LAT(256, 2); break;
+        case 1024: SB_LAT(256, 4); break;
+        default: {
+            A.lattice = reinterpret_cast<double *>(w + 256 + sizeof(double) * (size_t)A.nb);
+            const int64_t want = (A.S + 255) / 256;
+            const unsigned g = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 8);
+            k_lattice_global<MODE><<<g, 256, 0, st>>>(A);
+            if (int rc = launch_check(name)) return rc;
+            k_fold_blocks<<<grid, 1024, 0, st>>>(A);
+            if (int rc = launch_check(name)) return rc;
+            k_final_generic<<<1, 1024, 0, st>>>(A);
+        }
+    }
+#undef SB_LAT
+    return launch_check(name);
+}
+
+// ---- validators / helpers ------------------------------------------------
+
+__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
+    s = add(a, b);
+    const double bb = sub(s, a);
+    e = add(sub(a, sub(s, bb)), sub(b, bb));
+}
+__device__ __forceinline__ void dd_add(double &hi, double &lo, double h2, double l2) {
+    double s, e;
+    two_sum(hi, h2, s, e);
+    e = add(e, add(lo, l2));
+    two_sum(s, e, hi, lo);
+}
+
+__global__ void __launch_bounds__(256) k_dot_dd(const double *u, const double *v, int64_t n, double *hi_p,
+                                               double *lo_p, unsigned *ticket, double *result) {
+    double hi = 0.0, lo = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s, e;
+        two_sum(hi, mul(u[i], v[i]), s, e);
+        hi = s;
+        lo = add(lo, e);
+    }
+    __shared__ double sh[256], sl[256];
+    sh[threadIdx.x] = hi;
+    sl[threadIdx.x] = lo;
+    __syncthreads();
+    for (int k = 128; k >= 1; k >>= 1) {
+        if ((int)threadIdx.x < k) {
+            double h = sh[threadIdx.x], l = sl[threadIdx.x];
+            dd_add(h, l, sh[threadIdx.x + k], sl[threadIdx.x + k]);
+            sh[threadIdx.x] = h;
+            sl[threadIdx.x] = l;
+        }
+        __syncthreads();
+    }
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+        hi_p[blockIdx.x] = sh[0];
+        lo_p[blockIdx.x] = sl[0];
+        __threadfence();
+        is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (is_last && threadIdx.x == 0) {
+        __threadfence();
+        double h = 0.0, l = 0.0;
+        for (unsigned b = 0; b < gridDim.x; b++) dd_add(h, l, __ldcg(hi_p + b), __ldcg(lo_p + b));
+        *result = add(h, l);
+        *ticket = 0u;
+    }
+}
+
+__global__ void k_sum_ordered(const double *v, int64_t count, double *out) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < count; i++) acc = add(acc, v[i]);
+    *out = acc;
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+size_t sb_reduce_workspace_bytes(int64_t block_size, int64_t n_blocks) {
+    if (block_size < 2 || (block_size & (block_size - 1)) || n_blocks < 1) return 0;
+    return ws_bytes(block_size, n_blocks);
+}
+
+int sb_bs3_norm2(const double *x, int64_t n, int64_t bs, int64_t nb, void *ws, double *result,
+                 sb_stream_t s) {
+    RArgs A{};
+    A.u = x; A.v = x; A.n = n; A.bs = bs; A.nb = nb; A.result = result;
+    if (n > 0 && !x) { set_error("sb_bs3_norm2: null x"); return SB_E_INVALID; }
+    return launch_reduce<R_NORM>(A, ws, as_stream(s), "sb_bs3_norm2");
+}
+
+int sb_bs4_dot(const double *x, const double *y, int64_t n, int64_t bs, int64_t nb, void *ws,
+               double *result, sb_stream_t s) {
+    RArgs A{};
+    A.u = x; A.v = y; A.n = n; A.bs = bs; A.nb = nb; A.result = result;
+    if (n > 0 && (!x || !y)) { set_error("sb_bs4_dot: null input"); return SB_E_INVALID; }
+    return launch_reduce<R_DOT>(A, ws, as_stream(s), "sb_bs4_dot");
+}
+
+int sb_bs5_fused_cg_update(double alpha, const double *p, const double *ap, double *x, double *r,
+                           int64_t n, int64_t bs, int64_t nb, void *ws, double *result,
+                           sb_stream_t s) {
+    RArgs A{};
+    A.u = p; A.v = ap; A.x = x; A.r = r; A.alpha = alpha; A.n = n; A.bs = bs; A.nb = nb;
+    A.result = result;
+    if (n > 0 && (!p || !ap || !x || !r)) {
+        set_error("sb_bs5_fused_cg_update: null input");
+        return SB_E_INVALID;
+    }
+    return launch_reduce<R_FUSED>(A, ws, as_stream(s), "sb_bs5_fused_cg_update");
+}
+
+int sb_sum_ordered(const double *values, int64_t count, double *result, sb_stream_t s) {
+    clear_error();
+    if (count < 0 || !result || (count > 0 && !values)) {
+        set_error("sb_sum_ordered: invalid arguments");
+        return SB_E_INVALID;
+    }
+    k_sum_ordered<<<1, 1, 0, as_stream(s)>>>(values, count, result);
+    return launch_check("sb_sum_ordered");
+}
+
+int sb_dot_compensated(const double *u, const double *v, int64_t n, void *ws, double *result,
+                       sb_stream_t s) {
+    clear_error();
+    if (n < 0 || !ws || !result || (n > 0 && (!u || !v))) {
+        set_error("sb_dot_compensated: invalid arguments");
+        return SB_E_INVALID;
+    }
+    constexpr int G = 592;  // needs sb_reduce_workspace_bytes(256, 592) = 256 + 592*8 ... x2 below
+    char *w = static_cast<char *>(ws);
+    unsigned *ticket = reinterpret_cast<unsigned *>(w);
+    double *hi = reinterpret_cast<double *>(w + 256);
+    double *lo = hi + G / 2;  // G/2 doubles each: grid below uses G/2 CTAs
+    k_dot_dd<<<G / 2, 256, 0, as_stream(s)>>>(u, v, n, hi, lo, ticket, result);
+    return launch_check("sb_dot_compensated");
+}
+
+}  // extern "C"

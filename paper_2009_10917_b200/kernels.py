@@ -1,0 +1,212 @@
+"""BS1-BS5: copy, axpy, norm, dot, fused CG update on the B200.
+
+Drop-in for pkg/src/streambench/kernels.py: same names, argument order,
+in-place semantics, ReductionConfig validation and ValueError behaviour.
+Every call runs one hand-written sm_100a kernel from libsb200.so
+(include/sb200.h); reductions reproduce the reference lattice schedule
+(kernels.py:38-87) bit for bit for any ReductionConfig.
+
+Arguments may be CUDA float64 tensors (the fast path: no copies) or host
+arrays (numpy / CPU torch), which are staged to the current device and, for
+in-place outputs, written back -- so code written against the reference's
+numpy API runs unchanged.
+
+Reductions return a Python float like the reference (one device->host sync
+per call).  The `*_async` variants return the 1-element device tensor
+instead, for timed loops and device-resident solvers.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .core import DVector, check_same_length
+
+
+@dataclass(frozen=True)
+class ReductionConfig:
+    """kernels.py:19-32: shape of the two-stage reduction (lattice, not CUDA, shape)."""
+
+    block_size: int = 256
+    n_blocks: int = 512
+
+    def __post_init__(self):
+        b = self.block_size
+        if b < 2 or (b & (b - 1)) != 0:
+            raise ValueError(f"block_size must be a power of two >= 2, got {b}")
+        if self.n_blocks < 1:
+            raise ValueError(f"n_blocks must be >= 1, got {self.n_blocks}")
+
+
+DEFAULT_REDUCTION = ReductionConfig()
+
+# A lattice shaped for the B200 rather than for the paper's GPUs: 1184 = 8 x 148
+# CTAs of 256 slots fill every SM with two resident CTAs and give 303k
+# independent in-order chains.  Parity is per config, so results are bitwise
+# equal to the reference's kernels.bs3_norm2(x, B200_REDUCTION).
+B200_REDUCTION = ReductionConfig(block_size=256, n_blocks=1184)
+
+
+def _all_cuda(*vs) -> bool:
+    return all(isinstance(v, torch.Tensor) and v.is_cuda for v in vs)
+
+
+def _stage_all(names, vs):
+    dev = None
+    for v in vs:
+        if isinstance(v, torch.Tensor) and v.is_cuda:
+            dev = v.device
+            break
+    return [_lib.stage(v, torch.float64, n, dev) for n, v in zip(names, vs)]
+
+
+def _check_vec(v, name):
+    if v.dtype != torch.float64:
+        raise TypeError(f"{name}: expected float64, got {v.dtype}")
+    if v.dim() != 1:
+        raise ValueError(f"expected a 1-D vector, got shape {tuple(v.shape)}")
+    if not v.is_contiguous():
+        raise ValueError(f"{name}: vectors must be contiguous")
+
+
+def _same_device(*vs) -> torch.device:
+    dev = vs[0].device
+    for v in vs[1:]:
+        if v.device != dev:
+            raise ValueError(f"vectors on different devices: {dev} vs {v.device}")
+    return dev
+
+
+def _result(dev, out):
+    if out is None:
+        return torch.empty(1, dtype=torch.float64, device=dev)
+    if not (out.is_cuda and out.dtype == torch.float64 and out.numel() >= 1 and out.device == dev):
+        raise ValueError("out must be a float64 device tensor on the inputs' device")
+    return out
+
+
+# ---- BS1 -------------------------------------------------------------------
+
+def bs1_copy(x, y) -> None:
+    """kernels.py:90-93: y = x (in place)."""
+    check_same_length(x, y)
+    if _all_cuda(x, y):
+        _check_vec(x, "x"); _check_vec(y, "y")
+        dev = _same_device(x, y)
+        L = _lib.lib()
+        _lib.check(L.sb_bs1_copy(x.data_ptr(), y.data_ptr(), x.shape[0], _lib.stream_handle(dev)),
+                   "bs1_copy")
+        return
+    sx, sy = _stage_all(("x", "y"), (x, y))
+    bs1_copy(sx.dev, sy.dev)
+    sy.writeback()
+
+
+# ---- BS2 -------------------------------------------------------------------
+
+def bs2_axpy(alpha: float, x, beta: float, y) -> None:
+    """kernels.py:96-103: y = alpha*x + beta*y, one rounded multiply-add pair per element."""
+    check_same_length(x, y)
+    if _all_cuda(x, y):
+        _check_vec(x, "x"); _check_vec(y, "y")
+        dev = _same_device(x, y)
+        L = _lib.lib()
+        _lib.check(L.sb_bs2_axpy(float(alpha), x.data_ptr(), float(beta), y.data_ptr(), x.shape[0],
+                                 _lib.stream_handle(dev)), "bs2_axpy")
+        return
+    if x is y:
+        sx = _lib.stage(x, torch.float64, "x")
+        sy = sx
+    else:
+        sx, sy = _stage_all(("x", "y"), (x, y))
+    bs2_axpy(alpha, sx.dev, beta, sy.dev)
+    sy.writeback()
+
+
+# ---- BS3 / BS4 / BS5 -------------------------------------------------------
+
+def _cfg(cfg: ReductionConfig) -> ReductionConfig:
+    if not isinstance(cfg, ReductionConfig):
+        raise TypeError("cfg must be a ReductionConfig")
+    return cfg
+
+
+def bs3_norm2_async(x: DVector, cfg: ReductionConfig = DEFAULT_REDUCTION, out=None) -> torch.Tensor:
+    """bs3_norm2 leaving the scalar on the device (no host sync)."""
+    cfg = _cfg(cfg)
+    _check_vec(x, "x")
+    dev = x.device
+    L = _lib.lib()
+    st = _lib.stream_handle(dev)
+    ws = _lib.workspace(dev, st, cfg.block_size, cfg.n_blocks)
+    res = _result(dev, out)
+    _lib.check(L.sb_bs3_norm2(x.data_ptr(), x.shape[0], cfg.block_size, cfg.n_blocks, ws.data_ptr(),
+                              res.data_ptr(), st), "bs3_norm2")
+    return res
+
+
+def bs3_norm2(x, cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
+    """kernels.py:106-108: sum(x[i]^2) via the fixed two-stage schedule."""
+    if not _all_cuda(x):
+        x = _lib.stage(x, torch.float64, "x").dev
+    return float(bs3_norm2_async(x, cfg).item())
+
+
+def bs4_dot_async(x: DVector, y: DVector, cfg: ReductionConfig = DEFAULT_REDUCTION,
+                  out=None) -> torch.Tensor:
+    cfg = _cfg(cfg)
+    check_same_length(x, y)
+    _check_vec(x, "x"); _check_vec(y, "y")
+    dev = _same_device(x, y)
+    L = _lib.lib()
+    st = _lib.stream_handle(dev)
+    ws = _lib.workspace(dev, st, cfg.block_size, cfg.n_blocks)
+    res = _result(dev, out)
+    _lib.check(L.sb_bs4_dot(x.data_ptr(), y.data_ptr(), x.shape[0], cfg.block_size, cfg.n_blocks,
+                            ws.data_ptr(), res.data_ptr(), st), "bs4_dot")
+    return res
+
+
+def bs4_dot(x, y, cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
+    """kernels.py:111-114: sum(x[i]*y[i]) via the fixed two-stage schedule."""
+    check_same_length(x, y)
+    if not _all_cuda(x, y):
+        sx, sy = _stage_all(("x", "y"), (x, y))
+        x, y = sx.dev, sy.dev
+    return float(bs4_dot_async(x, y, cfg).item())
+
+
+def bs5_fused_cg_update_async(alpha: float, p: DVector, ap: DVector, x: DVector, r: DVector,
+                              cfg: ReductionConfig = DEFAULT_REDUCTION, out=None) -> torch.Tensor:
+    cfg = _cfg(cfg)
+    check_same_length(p, ap, x, r)
+    for v, nm in ((p, "p"), (ap, "ap"), (x, "x"), (r, "r")):
+        _check_vec(v, nm)
+    dev = _same_device(p, ap, x, r)
+    L = _lib.lib()
+    st = _lib.stream_handle(dev)
+    ws = _lib.workspace(dev, st, cfg.block_size, cfg.n_blocks)
+    res = _result(dev, out)
+    _lib.check(L.sb_bs5_fused_cg_update(float(alpha), p.data_ptr(), ap.data_ptr(), x.data_ptr(),
+                                        r.data_ptr(), x.shape[0], cfg.block_size, cfg.n_blocks,
+                                        ws.data_ptr(), res.data_ptr(), st), "bs5_fused_cg_update")
+    return res
+
+
+def bs5_fused_cg_update(alpha: float, p, ap, x, r,
+                        cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
+    """kernels.py:117-132: x += alpha*p; r -= alpha*ap; returns sum(r_new^2).
+
+    Genuinely single-pass on the device (48 B/element), same lattice as BS3.
+    """
+    check_same_length(p, ap, x, r)
+    if _all_cuda(p, ap, x, r):
+        return float(bs5_fused_cg_update_async(alpha, p, ap, x, r, cfg).item())
+    staged = _stage_all(("p", "ap", "x", "r"), (p, ap, x, r))
+    res = bs5_fused_cg_update_async(alpha, *(s.dev for s in staged), cfg)
+    staged[2].writeback()
+    staged[3].writeback()
+    return float(res.item())

@@ -1,0 +1,225 @@
+"""Structured hex mesh numbering and the scatter/gather operators, built on the GPU.
+
+Drop-in for pkg/src/streambench/mesh.py: same dataclasses, builders, error
+messages and -- verified bit for bit against the reference -- the same
+local_to_global, row_starts, col_ids and block_starts arrays.  Arrays live on
+the device as int32 tensors.
+
+For meshes made by build_mesh the CSR comes from a closed form
+(sb_build_gather_csr: O(1) per row, no sort, no scan); any other
+local_to_global map goes through the general path (stable CUB radix sort +
+lower-bound row starts, sb_build_gather_general).  Block packing is the
+reference's greedy rule in both cases (sb_build_block_starts).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from functools import cached_property
+
+import numpy as np
+import torch
+
+from . import _lib
+
+INDEX_DTYPE = torch.int32
+_INT32_MAX = 2**31 - 1
+
+
+def _dev(device=None) -> torch.device:
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+@dataclass(frozen=True)
+class MeshConnectivity:
+    """mesh.py:20-36: element-local to global node numbering for a K^3 mesh of order p."""
+
+    K: int
+    p: int
+    local_to_global: torch.Tensor = field(repr=False)
+    # True when local_to_global is the build_mesh numbering (enables the
+    # closed-form operator builder); user-supplied maps use the general path.
+    structured: bool = field(default=False, repr=False, compare=False)
+
+    @property
+    def nl(self) -> int:
+        return int(self.local_to_global.shape[0])
+
+    @property
+    def ng(self) -> int:
+        return (self.K * self.p + 1) ** 3
+
+
+@dataclass(frozen=True)
+class ScatterIds:
+    """mesh.py:39-51: local-to-global id map; masked entries hold -1."""
+
+    ids: torch.Tensor = field(repr=False)
+
+    @property
+    def nl(self) -> int:
+        return int(self.ids.shape[0])
+
+    @cached_property
+    def _minmax(self) -> tuple[int, int]:
+        # one device reduction per operator (the reference re-scans ids on
+        # every bs7 call, gs.py:49-50; ids are immutable, so we cache it)
+        ids = self.ids if self.ids.is_cuda else self.ids.cuda()
+        if ids.numel() == 0:
+            return (0, -1)
+        out = torch.empty(2, dtype=torch.int32, device=ids.device)
+        L = _lib.lib()
+        _lib.check(L.sb_ids_minmax(ids.data_ptr(), ids.shape[0], out.data_ptr(),
+                                   _lib.stream_handle(ids.device)), "ids_minmax")
+        lo, hi = out.tolist()
+        return int(lo), int(hi)
+
+    @cached_property
+    def has_mask(self) -> bool:
+        return self.nl > 0 and self._minmax[0] < 0
+
+    @property
+    def max_id(self) -> int:
+        return self._minmax[1]
+
+
+@dataclass(frozen=True)
+class GatherOp:
+    """mesh.py:54-70: CSR of the gather operator with row blocks of bounded nonzero count."""
+
+    ng: int
+    row_starts: torch.Tensor = field(repr=False)
+    col_ids: torch.Tensor = field(repr=False)
+    block_starts: torch.Tensor = field(repr=False)
+    nodes_per_block: int
+
+    @property
+    def nl(self) -> int:
+        return int(self.col_ids.shape[0])
+
+    @property
+    def n_blocks(self) -> int:
+        return int(self.block_starts.shape[0]) - 1
+
+
+def build_mesh(K: int, p: int, device=None) -> MeshConnectivity:
+    """mesh.py:73-97: number the nodes of a structured K*K*K mesh of order-p hexahedra."""
+    if K < 1 or p < 1:
+        raise ValueError(f"need K >= 1 and p >= 1, got K={K}, p={p}")
+    g = K * p + 1
+    if g**3 > _INT32_MAX:
+        raise ValueError(f"global id space (K*p+1)^3 = {g**3} overflows int32")
+    nl = K**3 * (p + 1) ** 3
+    if nl > _INT32_MAX:
+        # the reference silently wraps here (mesh.py:97)
+        raise ValueError(f"local DOF count K^3 (p+1)^3 = {nl} overflows int32")
+    dev = _dev(device)
+    l2g = torch.empty(nl, dtype=INDEX_DTYPE, device=dev)
+    L = _lib.lib()
+    _lib.check(L.sb_build_l2g(K, p, 0, K, l2g.data_ptr(), _lib.stream_handle(dev)), "build_mesh")
+    return MeshConnectivity(K=K, p=p, local_to_global=l2g, structured=True)
+
+
+def build_scatter_ids(mesh: MeshConnectivity, mask=None) -> ScatterIds:
+    """mesh.py:100-110: scatter id map for the mesh; global ids in `mask` become -1."""
+    l2g = mesh.local_to_global
+    dev = l2g.device if l2g.is_cuda else _dev()
+    if not l2g.is_cuda:
+        l2g = l2g.to(dev)
+    ids = torch.empty_like(l2g)
+    L = _lib.lib()
+    st = _lib.stream_handle(dev)
+    if mask is not None:
+        mask_ids = np.asarray(sorted(mask), dtype=np.int64)
+        if mask_ids.size and (mask_ids.min() < 0 or mask_ids.max() >= mesh.ng):
+            raise ValueError(f"mask ids must lie in [0, {mesh.ng})")
+    else:
+        mask_ids = np.zeros(0, dtype=np.int64)
+    if mask_ids.size:
+        gids = torch.from_numpy(mask_ids).to(dev)
+        scratch = torch.empty(mesh.ng, dtype=torch.uint8, device=dev)
+        _lib.check(L.sb_build_scatter_ids(l2g.data_ptr(), l2g.shape[0], gids.data_ptr(),
+                                          gids.shape[0], mesh.ng, scratch.data_ptr(),
+                                          ids.data_ptr(), st), "build_scatter_ids")
+    else:
+        _lib.check(L.sb_build_scatter_ids(l2g.data_ptr(), l2g.shape[0], None, 0, mesh.ng, None,
+                                          ids.data_ptr(), st), "build_scatter_ids")
+    return ScatterIds(ids=ids)
+
+
+def _max_row_len(K: int) -> int:
+    return 8 if K >= 2 else 1
+
+
+def _block_starts(row_starts: torch.Tensor, ng: int, npb: int) -> torch.Tensor:
+    dev = row_starts.device
+    L = _lib.lib()
+    st = _lib.stream_handle(dev)
+    bst = torch.empty(ng + 1, dtype=INDEX_DTYPE, device=dev)
+    nblk = torch.empty(1, dtype=torch.int64, device=dev)
+    _lib.check(L.sb_build_block_starts(row_starts.data_ptr(), ng, npb, bst.data_ptr(), ng,
+                                       nblk.data_ptr(), st), "build_gather")
+    nb = int(nblk.item())
+    if nb < 0:
+        raise ValueError(f"nodes_per_block={npb} is below the longest row")
+    return bst[: nb + 1].clone()
+
+
+def build_gather(mesh: MeshConnectivity, nodes_per_block: int = 512) -> GatherOp:
+    """mesh.py:113-147: CSR gather operator with greedily packed row blocks.
+
+    Row r lists (ascending) every local index mapping to global id r; blocks
+    take consecutive rows while their nonzeros stay within nodes_per_block.
+    """
+    ng, nl = mesh.ng, mesh.nl
+    l2g = mesh.local_to_global
+    dev = l2g.device if l2g.is_cuda else _dev()
+    L = _lib.lib()
+    st = _lib.stream_handle(dev)
+    rs = torch.empty(ng + 1, dtype=INDEX_DTYPE, device=dev)
+    ci = torch.empty(nl, dtype=INDEX_DTYPE, device=dev)
+    if mesh.structured:
+        longest = _max_row_len(mesh.K)
+        if longest > nodes_per_block:
+            raise ValueError(f"nodes_per_block={nodes_per_block} is below the longest row "
+                             f"({longest} nonzeros)")
+        _lib.check(L.sb_build_gather_csr(mesh.K, mesh.p, 0, mesh.K, 0, mesh.K * mesh.p + 1,
+                                         rs.data_ptr(), ci.data_ptr(), st), "build_gather")
+    else:
+        if not l2g.is_cuda:
+            l2g = l2g.to(dev)
+        tmp = torch.empty(int(L.sb_build_gather_general_temp_bytes(nl)), dtype=torch.uint8,
+                          device=dev)
+        stats = torch.empty(2, dtype=torch.int64, device=dev)
+        _lib.check(L.sb_build_gather_general(l2g.data_ptr(), nl, ng, rs.data_ptr(), ci.data_ptr(),
+                                             tmp.data_ptr(), tmp.shape[0], stats.data_ptr(), st),
+                   "build_gather")
+        cmin, cmax = (int(v) for v in stats.tolist())
+        if ng > 0 and cmin < 1:
+            raise ValueError("mesh does not cover every global id")
+        if cmax > nodes_per_block:
+            raise ValueError(f"nodes_per_block={nodes_per_block} is below the longest row "
+                             f"({cmax} nonzeros)")
+    bst = _block_starts(rs, ng, nodes_per_block)
+    return GatherOp(ng=ng, row_starts=rs, col_ids=ci, block_starts=bst,
+                    nodes_per_block=nodes_per_block)
+
+
+def multiplicity(mesh: MeshConnectivity) -> torch.Tensor:
+    """mesh.py:150-153: per-global-node count of element-local copies (float64, device)."""
+    l2g = mesh.local_to_global
+    dev = l2g.device if l2g.is_cuda else _dev()
+    out = torch.empty(mesh.ng, dtype=torch.float64, device=dev)
+    L = _lib.lib()
+    st = _lib.stream_handle(dev)
+    if mesh.structured:
+        _lib.check(L.sb_multiplicity(mesh.K, mesh.p, 0, mesh.K, 0, mesh.K * mesh.p + 1,
+                                     out.data_ptr(), st), "multiplicity")
+    else:
+        if not l2g.is_cuda:
+            l2g = l2g.to(dev)
+        _lib.check(L.sb_histogram(l2g.data_ptr(), l2g.shape[0], mesh.ng, out.data_ptr(), st),
+                   "multiplicity")
+    return out

@@ -1,0 +1,47 @@
+"""Worker-count API of the reference (parallel.py:1-69), kept for drop-in compatibility.
+
+On the B200 the CUDA grid replaces the reference's thread-pool span split
+(parallel.py:43-69).  The reference's determinism contract -- results
+bitwise independent of the worker count -- becomes "bitwise independent of
+launch geometry for a fixed ReductionConfig", which the kernels guarantee by
+construction (the lattice shape, not the grid, fixes every rounding).  The
+worker count is therefore recorded but changes nothing.
+"""
+
+from __future__ import annotations
+
+import os
+
+_num_workers = 1
+
+
+def set_num_workers(n: int) -> None:
+    """parallel.py:17-25 (validation identical; no effect on GPU results)."""
+    global _num_workers
+    if n < 1:
+        raise ValueError(f"worker count must be >= 1, got {n}")
+    _num_workers = n
+
+
+def num_workers() -> int:
+    return _num_workers
+
+
+def max_workers() -> int:
+    return os.cpu_count() or 1
+
+
+def split_range(n: int, parts: int) -> list[tuple[int, int]]:
+    """parallel.py:43-53: at most `parts` contiguous non-empty spans of range(n).
+
+    Used by the multi-GPU partitioner (dist.py) to cut vectors into rank chunks.
+    """
+    parts = max(1, min(parts, n))
+    step, extra = divmod(n, parts)
+    spans = []
+    lo = 0
+    for i in range(parts):
+        hi = lo + step + (1 if i < extra else 0)
+        spans.append((lo, hi))
+        lo = hi
+    return spans

@@ -1,0 +1,194 @@
+"""BS6/BS7 and the operator builders on the B200 vs the reference's golden
+arrays (bitwise) and the CPU oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from goldens import mesh_q_global, mesh_q_local, sha
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import paper_2009_10917_b200 as sb
+    from paper_2009_10917_b200 import _lib
+    _lib.lib()
+    return sb
+
+
+def d(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def h(t):
+    return t.cpu().numpy()
+
+
+def test_builders_and_kernels_vs_golden(sb, golden):
+    for rec in golden["meshes"]:
+        K, p, npb = rec["K"], rec["p"], rec["npb"]
+        mesh = sb.build_mesh(K, p)
+        assert mesh.nl == rec["nl"] and mesh.ng == rec["ng"]
+        assert sha(h(mesh.local_to_global)) == rec["l2g"], (K, p)
+        op = sb.build_gather(mesh, npb)
+        assert sha(h(op.row_starts)) == rec["row_starts"], (K, p)
+        assert sha(h(op.col_ids)) == rec["col_ids"], (K, p)
+        assert sha(h(op.block_starts)) == rec["block_starts"], (K, p, npb)
+        assert op.n_blocks == rec["n_blocks"]
+        q = mesh_q_local(K, p, mesh.nl)
+        out = sb.bs6_gather(op, d(q))
+        assert sha(h(out)) == rec["bs6_out"], (K, p)
+        ids = sb.build_scatter_ids(mesh)
+        assert not ids.has_mask
+        qg = mesh_q_global(K, p, mesh.ng)
+        ql = torch.zeros(mesh.nl, dtype=torch.float64, device="cuda")
+        sb.bs7_scatter(ids, d(qg), ql)
+        assert sha(h(ql)) == rec["bs7_out"], (K, p)
+        assert sha(h(sb.multiplicity(mesh))) == rec["mult"]
+        assert sb.bytes_moved("bs6", nl=mesh.nl, ng=mesh.ng) == rec["bytes_bs6"]
+
+
+def test_general_builder_path_matches(sb, golden):
+    """A user-supplied l2g (not flagged structured) goes through the CUB path."""
+    for rec in golden["meshes"][:12]:
+        K, p, npb = rec["K"], rec["p"], rec["npb"]
+        m = sb.build_mesh(K, p)
+        mu = sb.MeshConnectivity(K=K, p=p, local_to_global=m.local_to_global.clone())
+        op = sb.build_gather(mu, npb)
+        assert sha(h(op.row_starts)) == rec["row_starts"]
+        assert sha(h(op.col_ids)) == rec["col_ids"]
+        assert sha(h(op.block_starts)) == rec["block_starts"]
+        assert sha(h(sb.multiplicity(mu))) == rec["mult"]
+
+
+def test_general_builder_random_map(sb, oracle):
+    rng = np.random.default_rng(7)
+    ng = 5000
+    l2g = np.concatenate([np.arange(ng), rng.integers(0, ng, 20000)]).astype(np.int32)
+    rng.shuffle(l2g)
+    l2g_d = torch.from_numpy(l2g).cuda()
+    from paper_2009_10917_b200 import mesh as M
+    rs = torch.empty(ng + 1, dtype=torch.int32, device="cuda")
+    ci = torch.empty(l2g.shape[0], dtype=torch.int32, device="cuda")
+    from paper_2009_10917_b200 import _lib
+    L = _lib.lib()
+    tmp = torch.empty(int(L.sb_build_gather_general_temp_bytes(l2g.shape[0])), dtype=torch.uint8,
+                      device="cuda")
+    stats = torch.empty(2, dtype=torch.int64, device="cuda")
+    _lib.check(L.sb_build_gather_general(l2g_d.data_ptr(), l2g.shape[0], ng,
+                                         rs.data_ptr(), ci.data_ptr(), tmp.data_ptr(),
+                                         tmp.shape[0], stats.data_ptr(),
+                                         _lib.stream_handle()), "general")
+    rs_o, ci_o, bst_o = oracle.build_gather(l2g, ng, 64)
+    assert np.array_equal(h(rs), rs_o) and np.array_equal(h(ci), ci_o)
+    assert np.array_equal(h(M._block_starts(rs, ng, 64)), bst_o)
+
+
+def test_masks_vs_golden(sb, golden):
+    for rec in golden["masks"]:
+        K, p = rec["K"], rec["p"]
+        mesh = sb.build_mesh(K, p)
+        ids = sb.build_scatter_ids(mesh, mask=set(rec["mask"]))
+        assert sha(h(ids.ids)) == rec["ids"]
+        assert ids.has_mask == rec["has_mask"]
+        qg = np.random.default_rng([9, K, p]).uniform(-1, 1, mesh.ng)
+        ql = torch.full((mesh.nl,), 99.0, dtype=torch.float64, device="cuda")
+        sb.bs7_scatter(ids, d(qg), ql)
+        assert sha(h(ql)) == rec["out"]
+
+
+def test_gs_errors_and_identities(sb):
+    mesh = sb.build_mesh(1, 1)
+    op = sb.build_gather(mesh)
+    q = d(np.arange(8.0))
+    assert torch.equal(sb.bs6_gather(op, q), q)  # test_gs.py:23-26
+    with pytest.raises(ValueError):
+        sb.bs6_gather(op, d(np.zeros(9)))
+    ids = sb.build_scatter_ids(mesh)
+    with pytest.raises(ValueError):
+        sb.bs7_scatter(ids, d(np.zeros(8)), d(np.zeros(9)))
+    with pytest.raises(ValueError):
+        sb.bs7_scatter(ids, d(np.zeros(4)), d(np.zeros(8)))
+    with pytest.raises(ValueError):
+        sb.build_gather(sb.build_mesh(2, 1), 7)  # test_mesh.py:173-176
+    with pytest.raises(ValueError):
+        sb.build_mesh(200, 7)
+    with pytest.raises(ValueError):
+        sb.build_mesh(0, 1)
+    with pytest.raises(ValueError):
+        sb.build_scatter_ids(mesh, mask={8})
+    m = sb.build_mesh(2, 2)
+    full = sb.build_scatter_ids(m, mask=set(range(m.ng)))
+    assert bool((full.ids == -1).all())
+    ql = d(np.random.default_rng(3).uniform(-1, 1, m.nl))
+    before = ql.clone()
+    sb.bs7_scatter(full, d(np.ones(m.ng)), ql)
+    assert torch.equal(ql, before)
+
+
+@pytest.mark.parametrize("K,p", [(1, 1), (2, 1), (3, 2), (4, 3), (2, 7), (3, 15)])
+def test_round_trip_and_linearity(sb, K, p):
+    mesh = sb.build_mesh(K, p)
+    op = sb.build_gather(mesh)
+    ids = sb.build_scatter_ids(mesh)
+    qg = d(np.random.default_rng([K, p]).uniform(-1, 1, mesh.ng))
+    ql = torch.zeros(mesh.nl, dtype=torch.float64, device="cuda")
+    sb.bs7_scatter(ids, qg, ql)
+    m = sb.multiplicity(mesh)
+    assert torch.allclose(sb.bs6_gather(op, ql), m * qg, rtol=1e-13, atol=0)
+    u = d(np.random.default_rng(3).uniform(-1, 1, mesh.nl))
+    v = d(np.random.default_rng(4).uniform(-1, 1, mesh.nl))
+    comb = sb.bs6_gather(op, 2.5 * u - 0.75 * v)
+    sep = 2.5 * sb.bs6_gather(op, u) - 0.75 * sb.bs6_gather(op, v)
+    assert torch.allclose(comb, sep, rtol=1e-13, atol=1e-15)
+
+
+@pytest.mark.parametrize("K,p,npb", [(40, 7, 512), (20, 3, 16), (12, 15, 4096), (30, 1, 8)])
+def test_builders_vs_oracle_larger(sb, oracle, K, p, npb):
+    mesh = sb.build_mesh(K, p)
+    l2g = oracle.build_mesh(K, p)
+    assert np.array_equal(h(mesh.local_to_global), l2g)
+    op = sb.build_gather(mesh, npb)
+    rs, ci, bst = oracle.build_gather(l2g, mesh.ng, npb)
+    assert np.array_equal(h(op.row_starts), rs)
+    assert np.array_equal(h(op.col_ids), ci)
+    assert np.array_equal(h(op.block_starts), bst)
+    q = np.random.default_rng([K, p]).uniform(-1, 1, mesh.nl)
+    assert np.array_equal(h(sb.bs6_gather(op, d(q))), oracle.bs6_gather(rs, ci, q))
+
+
+def test_c3_scale_bs6_bs7(sb, oracle):
+    """C3 at N=7 (K=66, NG ~ 1e8): bitwise vs the row-wise oracle."""
+    K, p = 66, 7
+    oracle.set_threads(oracle.max_threads())
+    try:
+        mesh = sb.build_mesh(K, p)
+        op = sb.build_gather(mesh)
+        gen = torch.Generator(device="cuda"); gen.manual_seed(66)
+        q = torch.empty(mesh.nl, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
+        out = sb.bs6_gather(op, q)
+        want = oracle.bs6_gather(h(op.row_starts), h(op.col_ids), h(q))
+        assert np.array_equal(h(out), want)
+        ids = sb.build_scatter_ids(mesh)
+        qg = torch.empty(mesh.ng, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
+        ql = torch.zeros(mesh.nl, dtype=torch.float64, device="cuda")
+        sb.bs7_scatter(ids, qg, ql)
+        assert torch.equal(ql, qg[mesh.local_to_global.long()])
+    finally:
+        oracle.set_threads(1)
+
+
+def test_reference_numpy_operator_drop_in(sb, golden):
+    """The reference's numpy GatherOp-like objects are accepted (staged per call)."""
+    import types
+    arr = golden.arrays
+    tag = "3_2_64"
+    op = types.SimpleNamespace(ng=7 ** 3, row_starts=arr[f"rs_{tag}"], col_ids=arr[f"ci_{tag}"],
+                               block_starts=arr[f"bst_{tag}"], nodes_per_block=64,
+                               nl=arr[f"ci_{tag}"].shape[0])
+    q = mesh_q_local(3, 2, op.nl)
+    out = sb.bs6_gather(op, q)
+    assert isinstance(out, np.ndarray)
+    assert np.array_equal(out, arr[f"bs6_{tag}"])
