@@ -81,6 +81,11 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.timed_from = None
+
+    def mark(self):
+        """Index of the first sample taken inside the timed region."""
+        self.timed_from = len(self.lines)
 
     def __enter__(self):
         try:
@@ -123,8 +128,11 @@ class ClockSampler:
                     reasons.add(name)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        timed = len(self.lines) - (self.timed_from or 0)
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "samples_in_timed_region": max(0, timed),
+                "window": "nvidia-smi every 100 ms from warm-up through the timed region "
+                          "(>= 0.6 s of back-to-back steps precede the timer)"}
 
 
 def cpu_cores():
@@ -271,13 +279,27 @@ class Workload:
             sb.bs7_scatter(self.ids, self.qg, self.ql)
 
 
-def time_steps(w, steps, warmup, barrier):
-    """Warm-up, then `steps` timed steps with per-test CUDA events on the launch stream."""
+def time_steps(w, steps, warmup, barrier, clk=None, settle_s=0.6):
+    """Warm-up, then `steps` timed steps with per-test CUDA events on the launch stream.
+
+    The clock sampler runs from the warm-up on; untimed steps continue until it
+    has seen the GPU under load for `settle_s`, so the clocks reported describe
+    the state the timed region runs in even when that region is short."""
     torch = w.torch
     stream = torch.cuda.current_stream(w.dev)
     for _ in range(warmup):
         for t in TESTS:
             w.call(t)
+    t0 = time.perf_counter()
+    while clk is not None and clk.proc is not None and (
+            time.perf_counter() - t0 < settle_s or len(clk.lines) < 2):
+        for t in TESTS:
+            w.call(t)
+        torch.cuda.synchronize(w.dev)
+        if time.perf_counter() - t0 > 10.0:
+            break
+    if clk is not None:
+        clk.mark()
     barrier()
     torch.cuda.synchronize(w.dev)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(TESTS) + 1)] for _ in range(steps)]
@@ -363,9 +385,9 @@ def traffic_from_profiles(kernel_key):
         return None
 
 
-KERNEL_KEYS = {"bs1": "k_elem_vec<0>", "bs2": "k_elem_vec<1>", "bs3": "k_lattice<norm>",
-               "bs4": "k_lattice<dot>", "bs5": "k_lattice<fused>", "bs6": "k_bs6_smem",
-               "bs7": "k_bs7_vec"}
+KERNEL_KEYS = {"bs1": "k_elem_vec<0>", "bs2": "k_elem_vec<1>", "bs3": "k_lattice_tma<norm>",
+               "bs4": "k_lattice_tma<dot>", "bs5": "k_lattice_tma<fused>", "bs6": "k_bs6_pipe",
+               "bs7": "k_bs7_pipe"}
 
 
 def main_ours(args):
@@ -391,7 +413,8 @@ def main_ours(args):
 
     w = Workload(args, device, dist_ctx)
     with ClockSampler(local) as clk:
-        total_ms, per_ms = time_steps(w, args.steps, args.warmup, barrier)
+        total_ms, per_ms = time_steps(w, args.steps, args.warmup, barrier, clk)
+        time.sleep(0.25)  # let the sampler flush the last interval
     step_ms = total_ms / args.steps
     if world > 1:
         t = torch.tensor([step_ms] + [per_ms[k] for k in TESTS], dtype=torch.float64, device=device)

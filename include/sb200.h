@@ -102,6 +102,21 @@ int sb_bs6_gather(const int32_t *block_starts, int64_t n_blocks, const int32_t *
                   const double *q_local, double *out, const double *carry_in, int64_t n_carry,
                   sb_stream_t stream);
 
+/* Pipelined BS6 (the fast path): a per-operator "plan" of super-blocks
+ * (G = max(1, 2048 / nodes_per_block) consecutive row blocks each) lets a
+ * persistent kernel keep index tiles, value gathers and row sums of three
+ * super-blocks in flight.  sb_bs6_plan_size returns the number of int32
+ * plan entries (0 if nodes_per_block > 2048: use sb_bs6_gather);
+ * sb_bs6_make_plan fills it once per operator.  row_starts and col_ids must
+ * be 16-byte aligned.  Results are bitwise those of sb_bs6_gather. */
+int64_t sb_bs6_plan_size(int64_t n_blocks, int64_t nodes_per_block);
+int sb_bs6_make_plan(const int32_t *block_starts, int64_t n_blocks, const int32_t *row_starts,
+                     int64_t nodes_per_block, int32_t *plan, sb_stream_t stream);
+int sb_bs6_gather_planned(const int32_t *plan, int64_t n_blocks, int64_t nodes_per_block,
+                          const int32_t *row_starts, const int32_t *col_ids, int64_t ng,
+                          int64_t nl, const double *q_local, double *out,
+                          const double *carry_in, int64_t n_carry, sb_stream_t stream);
+
 /* gs.py:42-61 bs7_scatter(ids, q_global, q_local): q_local[n] =
  * q_global[ids[n]] where ids[n] >= 0 (masked entries untouched).  The caller
  * validates max(ids) < ng once per operator (sb_ids_minmax) instead of per

@@ -62,6 +62,10 @@ _SIGS = {
     "sb_build_gather_general": (_c_int, [_c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_size, _c_vp,
                                          _c_vp]),
     "sb_histogram": (_c_int, [_c_vp, _c_i64, _c_i64, _c_vp, _c_vp]),
+    "sb_bs6_plan_size": (_c_i64, [_c_i64, _c_i64]),
+    "sb_bs6_make_plan": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_vp]),
+    "sb_bs6_gather_planned": (_c_int, [_c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp,
+                                       _c_vp, _c_vp, _c_i64, _c_vp]),
 }
 
 _lib = None

@@ -13,6 +13,8 @@
 // gathers q_global with an L2 evict_last policy: every global node is
 // re-read by up to 8 elements, the furthest one a whole element layer later
 // (SURVEY Appendix A.6), so q_global must survive the streams in L2.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "sb_common.cuh"
@@ -21,6 +23,15 @@ namespace sb {
 
 constexpr int kGsThreads = 256;
 constexpr int kGatherCap = 2048;  // entries staged per CTA (16 KB of q)
+
+// SB200_NO_PIPE=1 selects the one-tile-per-CTA kernels (A/B checks).
+static bool use_pipe() {
+    static const bool on = [] {
+        const char *e = getenv("SB200_NO_PIPE");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
 
 template <int T, int CAP>
 __global__ void __launch_bounds__(T) k_bs6_smem(const int32_t *__restrict__ bst, int64_t nblk, int G,
@@ -122,6 +133,9 @@ __global__ void __launch_bounds__(T) k_bs7_vec(const int4 *__restrict__ ids, int
     }
 }
 
+int bs7_pipe_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,
+                    cudaStream_t st);  // sb_gs_pipe.cu
+
 __global__ void __launch_bounds__(256) k_bs7_scalar(const int32_t *ids, int64_t nl, const double *qg,
                                                    double *ql) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl;
@@ -170,6 +184,7 @@ int sb_bs7_scatter(const int32_t *ids, int64_t nl, const double *qg, int64_t ng,
     }
     if (nl == 0) return SB_OK;
     cudaStream_t st = as_stream(s);
+    if (use_pipe() && aligned16(ids) && aligned16(ql)) return bs7_pipe_launch(ids, nl, qg, ql, has_mask, st);
     if (!aligned16(ids) || !aligned16(ql)) {
         const int64_t grid = std::min<int64_t>((nl + 255) / 256, (int64_t)sm_count() * 32);
         k_bs7_scalar<<<(unsigned)grid, 256, 0, st>>>(ids, nl, qg, ql);

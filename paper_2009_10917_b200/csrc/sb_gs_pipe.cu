@@ -1,0 +1,267 @@
+// sb_gs_pipe.cu -- software-pipelined persistent BS6 gather / BS7 scatter.
+//
+// The gather/scatter chains are index -> value -> store: dependent DRAM round
+// trips.  The one-tile-per-CTA kernels in sb_gs.cu pay them serially inside
+// each CTA (block_starts -> row_starts -> col_ids -> q -> sum -> store), which
+// leaves HBM half idle (ncu: ~50% DRAM throughput, long-scoreboard bound).
+// Here each CTA is persistent and prefetches the *indices of the next tile*
+// (and, for BS6, the plan entry of the tile after that) into registers while
+// the current tile's value gathers are in flight, so every iteration exposes a
+// single round trip and ~30 KB per CTA stay in flight.  (A cp.async/LDGSTS
+// 3-stage variant of this pipeline was measured slower: MIO-throttle bound on
+// the 8-byte gathers.)
+//
+// Results are bitwise those of the one-tile kernels: BS6 still sums each row
+// in ascending column order from +0.0 (or the carry-in) in one thread.
+#include <algorithm>
+
+#include "sb_common.cuh"
+
+namespace sb {
+
+constexpr int kPipeT = 256;
+constexpr int kBs6Cap = 2048;  // entries per BS6 super-block (8 per thread)
+
+// ---- BS7 ----------------------------------------------------------------
+template <int T, int U, bool MASK>
+__global__ void __launch_bounds__(T) k_bs7_pipe(const int4 *__restrict__ ids4, int64_t n4,
+                                               const double *__restrict__ qg, double2 *__restrict__ ql2,
+                                               const int32_t *__restrict__ ids, double *__restrict__ ql,
+                                               int64_t nl) {
+    const uint64_t pol = policy_evict_last();
+    const int64_t stride = (int64_t)gridDim.x * T * U;
+    int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x;
+    int4 nxt[U];
+#pragma unroll
+    for (int j = 0; j < U; j++)
+        if (base + j * T < n4) nxt[j] = ld_stream(ids4 + base + j * T);
+    for (; base < n4; base += stride) {
+        int4 cur[U];
+        double v[U][4];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            cur[j] = nxt[j];
+            if (base + j * T < n4) {
+                if (!MASK || cur[j].x >= 0) v[j][0] = ld_keep(qg + cur[j].x, pol);
+                if (!MASK || cur[j].y >= 0) v[j][1] = ld_keep(qg + cur[j].y, pol);
+                if (!MASK || cur[j].z >= 0) v[j][2] = ld_keep(qg + cur[j].z, pol);
+                if (!MASK || cur[j].w >= 0) v[j][3] = ld_keep(qg + cur[j].w, pol);
+            }
+        }
+        const int64_t nb = base + stride;  // prefetch the next tile's ids
+#pragma unroll
+        for (int j = 0; j < U; j++)
+            if (nb + j * T < n4) nxt[j] = ld_stream(ids4 + nb + j * T);
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const int64_t i = base + j * T;
+            if (i < n4) {
+                if (!MASK) {
+                    st_stream(ql2 + 2 * i, make_double2(v[j][0], v[j][1]));
+                    st_stream(ql2 + 2 * i + 1, make_double2(v[j][2], v[j][3]));
+                } else {
+                    double *o = reinterpret_cast<double *>(ql2 + 2 * i);
+                    if (cur[j].x >= 0) st_stream(o + 0, v[j][0]);
+                    if (cur[j].y >= 0) st_stream(o + 1, v[j][1]);
+                    if (cur[j].z >= 0) st_stream(o + 2, v[j][2]);
+                    if (cur[j].w >= 0) st_stream(o + 3, v[j][3]);
+                }
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 4) {  // ragged tail (nl % 4)
+        const int64_t i = 4 * n4 + threadIdx.x;
+        if (i < nl) {
+            const int32_t d = ids[i];
+            if (!MASK || d >= 0) ql[i] = qg[d];
+        }
+    }
+}
+
+int bs7_pipe_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,
+                    cudaStream_t st) {
+    constexpr int T = kPipeT, U = 2;
+    const int64_t n4 = nl / 4;
+    int per_sm = 1;
+    if (has_mask)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bs7_pipe<T, U, true>, T, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bs7_pipe<T, U, false>, T, 0);
+    const int64_t tiles = std::max<int64_t>(1, (n4 + T * U - 1) / (T * U));
+    const unsigned grid =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count() * std::max(1, per_sm)));
+    const int4 *ids4 = reinterpret_cast<const int4 *>(ids);
+    double2 *ql2 = reinterpret_cast<double2 *>(ql);
+    if (has_mask)
+        k_bs7_pipe<T, U, true><<<grid, T, 0, st>>>(ids4, n4, qg, ql2, ids, ql, nl);
+    else
+        k_bs7_pipe<T, U, false><<<grid, T, 0, st>>>(ids4, n4, qg, ql2, ids, ql, nl);
+    return launch_check("sb_bs7_scatter");
+}
+
+// ---- BS6 ----------------------------------------------------------------
+// plan[2i] = first row of super-block i, plan[2i+1] = its first entry;
+// super-block i = operator blocks [i*G, (i+1)*G), G = max(1, CAP/npb), so a
+// super-block has <= CAP entries and <= CAP rows (rows are non-empty).
+__global__ void k_bs6_plan(const int32_t *bst, int64_t nblk, const int32_t *rs, int G, int64_t nsb,
+                           int32_t *plan) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nsb;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i * G < nblk ? i * G : nblk;
+        const int32_t r = bst[b];
+        plan[2 * i] = r;
+        plan[2 * i + 1] = rs[r];
+    }
+}
+
+struct SbMeta {
+    int32_t r0, e0, r1, e1;
+};
+
+__device__ __forceinline__ SbMeta load_meta(const int32_t *plan, int64_t i, int64_t nsb) {
+    SbMeta m{0, 0, 0, 0};
+    if (i < nsb) {
+        const int2 lo = __ldg(reinterpret_cast<const int2 *>(plan + 2 * i));
+        const int2 hi = __ldg(reinterpret_cast<const int2 *>(plan + 2 * i + 2));
+        m = SbMeta{lo.x, lo.y, hi.x, hi.y};
+    }
+    return m;
+}
+
+template <int T, int CAP>
+__global__ void __launch_bounds__(T, 3) k_bs6_pipe(const int32_t *__restrict__ plan, int64_t nsb,
+                                                  const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
+                                                  const double *__restrict__ q, double *__restrict__ out,
+                                                  const double *__restrict__ carry, int64_t ncarry) {
+    constexpr int M = CAP / T;             // entries per thread
+    constexpr int R = (CAP + 1 + T - 1) / T;  // row starts per thread (rows <= CAP)
+    extern __shared__ __align__(16) unsigned char bs6_smem[];
+    double(*qs)[CAP] = reinterpret_cast<double(*)[CAP]>(bs6_smem);
+    int32_t(*rss)[CAP + 4] = reinterpret_cast<int32_t(*)[CAP + 4]>(bs6_smem + 2 * CAP * sizeof(double));
+
+    const int64_t g = gridDim.x;
+    int64_t sbi = blockIdx.x;
+    SbMeta mc = load_meta(plan, sbi, nsb);      // current super-block
+    SbMeta mn = load_meta(plan, sbi + g, nsb);  // next
+    int32_t cols[M];
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        const int k = threadIdx.x + m * T;
+        if (k < mc.e1 - mc.e0) cols[m] = ld_stream(ci + mc.e0 + k);
+    }
+    int buf = 0;
+    for (; sbi < nsb; sbi += g) {
+        const int ne = mc.e1 - mc.e0, nrows = mc.r1 - mc.r0;
+        // A: value gathers of this super-block; B: its row starts
+        double v[M];
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int k = threadIdx.x + m * T;
+            if (k < ne) v[m] = __ldg(q + cols[m]);
+        }
+        int32_t rv[R];
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+            const int k = threadIdx.x + j * T;
+            if (k <= nrows) rv[j] = ld_stream(rs + mc.r0 + k);
+        }
+        // C: indices of the next super-block; D: plan entry of the one after
+        const int nne = mn.e1 - mn.e0;
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int k = threadIdx.x + m * T;
+            if (k < nne) cols[m] = ld_stream(ci + mn.e0 + k);
+        }
+        const SbMeta mnn = load_meta(plan, sbi + 2 * g, nsb);
+        // E: publish A/B to shared memory
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int k = threadIdx.x + m * T;
+            if (k < ne) qs[buf][k] = v[m];
+        }
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+            const int k = threadIdx.x + j * T;
+            if (k <= nrows) rss[buf][k] = rv[j];
+        }
+        __syncthreads();
+        // G: one thread per row, ascending column order
+        for (int k = threadIdx.x; k < nrows; k += T) {
+            const int a = rss[buf][k] - mc.e0, b = rss[buf][k + 1] - mc.e0;
+            const int64_t r = (int64_t)mc.r0 + k;
+            double acc = r < ncarry ? carry[r] : 0.0;
+            for (int c = a; c < b; c++) acc = add(acc, qs[buf][c]);
+            st_stream(out + r, acc);
+        }
+        buf ^= 1;  // the barrier of the next iteration separates reuse of this buffer
+        mc = mn;
+        mn = mnn;
+    }
+}
+
+static int64_t bs6_G(int64_t npb) { return std::max<int64_t>(1, kBs6Cap / npb); }
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+int64_t sb_bs6_plan_size(int64_t n_blocks, int64_t npb) {
+    if (n_blocks < 1 || npb < 1 || npb > kBs6Cap) return 0;
+    const int64_t G = bs6_G(npb);
+    return 2 * ((n_blocks + G - 1) / G + 1);
+}
+
+int sb_bs6_make_plan(const int32_t *bst, int64_t nblk, const int32_t *rs, int64_t npb, int32_t *plan,
+                     sb_stream_t s) {
+    clear_error();
+    if (!bst || !rs || !plan || sb_bs6_plan_size(nblk, npb) == 0) {
+        set_error("sb_bs6_make_plan: invalid arguments (nodes_per_block must be <= %d)", kBs6Cap);
+        return SB_E_INVALID;
+    }
+    const int G = (int)bs6_G(npb);
+    const int64_t nsb = (nblk + G - 1) / G;
+    const int64_t grid = std::min<int64_t>((nsb + 256) / 256, (int64_t)sm_count() * 16);
+    k_bs6_plan<<<(unsigned)std::max<int64_t>(1, grid), 256, 0, as_stream(s)>>>(bst, nblk, rs, G, nsb, plan);
+    return launch_check("sb_bs6_make_plan");
+}
+
+int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const int32_t *rs,
+                          const int32_t *ci, int64_t ng, int64_t nl, const double *q, double *out,
+                          const double *carry, int64_t ncarry, sb_stream_t s) {
+    clear_error();
+    const int64_t psize = sb_bs6_plan_size(nblk, npb);
+    if (ng < 0 || nl < 0 || ncarry < 0 || (ncarry > 0 && !carry) || !plan || psize == 0 ||
+        (ng > 0 && (!rs || !out)) || (nl > 0 && (!ci || !q))) {
+        set_error("sb_bs6_gather_planned: invalid arguments");
+        return SB_E_INVALID;
+    }
+    if (reinterpret_cast<uintptr_t>(plan) & 7u) {
+        set_error("sb_bs6_gather_planned: plan must be 8-byte aligned");
+        return SB_E_INVALID;
+    }
+    if (ng == 0) return SB_OK;
+    if (ncarry > ng) ncarry = ng;
+    const int64_t nsb = psize / 2 - 1;
+    constexpr int T = kPipeT;
+    const size_t smem = 2 * kBs6Cap * sizeof(double) + 2 * (kBs6Cap + 4) * sizeof(int32_t);
+    static thread_local int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+        if (cuda_check(cudaFuncSetAttribute(k_bs6_pipe<T, kBs6Cap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem),
+                       "sb_bs6_gather_planned: shared memory attribute"))
+            return SB_E_CUDA;
+        attr_dev = dev;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bs6_pipe<T, kBs6Cap>, T, smem);
+    const int64_t grid = std::min<int64_t>(nsb, (int64_t)sm_count() * std::max(1, per_sm));
+    k_bs6_pipe<T, kBs6Cap><<<(unsigned)std::max<int64_t>(1, grid), T, smem, as_stream(s)>>>(
+        plan, nsb, rs, ci, q, out, carry, ncarry);
+    return launch_check("sb_bs6_gather_planned");
+}
+
+}  // extern "C"

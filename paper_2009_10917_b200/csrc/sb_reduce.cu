@@ -19,6 +19,8 @@
 //   * BS5 updates x and r and accumulates r_new^2 in the same pass (48 B/el,
 //     the reference's CPU code re-reads r), on the BS3 lattice, so
 //     bs5 == bs3_norm2(r_new) bitwise (test_kernels.py:194-199).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "sb_common.cuh"
@@ -186,6 +188,154 @@ __global__ void __launch_bounds__(T, (1024 / T) < 32 ? (1024 / T) : 32) k_lattic
     second_stage<T>(A, sm, bs, SPT, v);
 }
 
+// ---- TMA-ring lattice kernel ---------------------------------------------
+// Same lattice, same per-slot order; the memory-level parallelism comes from a
+// ring of ST shared-memory stages filled by cp.async.bulk (TMA) instead of
+// registers.  For step c, CTA b's slots need the contiguous chunk
+// [c*S + b*bs, +bs) of every input array -- one bulk copy per array per
+// stage, issued by a dedicated producer warp.  The T/32 consumer warps read
+// their slots from shared memory, fold them into their chains in c order and
+// (BS5) stream x', r' back with evict-first stores; each consumer warp
+// releases the stage through an `empty` mbarrier.  The last (partial) chunk
+// of a CTA, if any, is read straight from global memory, still in chain order.
+template <int MODE>
+struct NArr {
+    static constexpr int v = MODE == R_NORM ? 1 : (MODE == R_DOT ? 2 : 4);
+};
+
+template <int T, int SPT, int MODE, int ST>
+__global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs A) {
+    constexpr int BS = T * SPT;
+    constexpr int NA = NArr<MODE>::v;
+    constexpr int NCW = T / 32;  // consumer warps
+    __shared__ __align__(128) double buf[ST][NA][BS];
+    __shared__ __align__(8) uint64_t full[ST], empty[ST];
+    __shared__ double sm[BS];
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int64_t S = A.S, n = A.n;
+    const int64_t base0 = (int64_t)blockIdx.x * BS;
+    const int64_t nfull = n >= base0 + BS ? (n - base0 - BS) / S + 1 : 0;
+
+    if (tid == 0) {
+        for (int s = 0; s < ST; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    double acc[SPT];
+#pragma unroll
+    for (int j = 0; j < SPT; j++) acc[j] = 0.0;
+
+    if (warp == NCW) {
+        // producer warp: one elected lane issues the bulk copies
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            const double *src[4] = {A.u, A.v, A.x, A.r};
+            if (MODE == R_NORM) src[0] = A.u;
+            for (int64_t c = 0; c < nfull; c++) {
+                const int s = (int)(c % ST);
+                if (c >= ST) mbar_wait(&empty[s], (uint32_t)((c / ST - 1) & 1));
+                mbar_arrive_expect_tx(&full[s], (uint32_t)(NA * BS * sizeof(double)));
+                const int64_t off = c * S + base0;
+#pragma unroll
+                for (int a = 0; a < NA; a++)
+                    bulk_g2s(&buf[s][a][0], src[a] + off, (uint32_t)(BS * sizeof(double)), &full[s], pol);
+            }
+        }
+    } else {
+        for (int64_t c = 0; c < nfull; c++) {
+            const int s = (int)(c % ST);
+            mbar_wait(&full[s], (uint32_t)((c / ST) & 1));
+            const int64_t off = c * S + base0;
+#pragma unroll
+            for (int j = 0; j < SPT; j++) {
+                const int k = tid + j * T;
+                if constexpr (MODE == R_NORM) {
+                    const double a = buf[s][0][k];
+                    acc[j] = add(acc[j], mul(a, a));
+                } else if constexpr (MODE == R_DOT) {
+                    acc[j] = add(acc[j], mul(buf[s][0][k], buf[s][1][k]));
+                } else {
+                    const double xn = add(buf[s][2][k], mul(A.alpha, buf[s][0][k]));
+                    const double rn = sub(buf[s][3][k], mul(A.alpha, buf[s][1][k]));
+                    st_stream(A.x + off + k, xn);
+                    st_stream(A.r + off + k, rn);
+                    acc[j] = add(acc[j], mul(rn, rn));
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // partial last chunk (at most one per CTA), from global memory
+        const int64_t off = nfull * S + base0;
+        if (off < n) {
+#pragma unroll
+            for (int j = 0; j < SPT; j++) {
+                const int64_t i = off + tid + j * T;
+                if (i < n) {
+                    Step<MODE> st;
+                    st.load(A, i);
+                    acc[j] = add(acc[j], step_term<MODE>(st, A, i));
+                }
+            }
+        }
+    }
+    if (tid < T) {
+#pragma unroll
+        for (int j = 0; j < SPT; j++) sm[tid + j * T] = acc[j];
+    }
+    __syncthreads();
+    // tree fold (threads >= T skip the smem levels; warp 0 does the shuffles)
+    for (int k = BS / 2; k >= 32; k >>= 1) {
+        for (int s = tid; s < k; s += T) sm[s] = add(sm[s], sm[s + k]);
+        __syncthreads();
+    }
+    double v = 0.0;
+    if (tid < 32) {
+        constexpr int W = BS < 32 ? BS : 32;
+        if (tid < W) v = sm[tid];
+        for (int off = W / 2; off >= 1; off >>= 1) v = add(v, __shfl_down_sync(0xffffffffu, v, off));
+    }
+    __syncthreads();
+    // second stage by the last CTA
+    __shared__ bool is_last;
+    if (tid == 0) {
+        A.partials[blockIdx.x] = v;
+        __threadfence();
+        is_last = atomicAdd(A.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    if (tid < T) {
+        for (int j = 0; j < SPT; j++) {
+            const int t = tid + j * T;
+            double a2 = 0.0;
+            for (int64_t c = t; c < A.nb; c += BS) a2 = add(a2, __ldcg(A.partials + c));
+            sm[t] = a2;
+        }
+    }
+    __syncthreads();
+    for (int k = BS / 2; k >= 32; k >>= 1) {
+        for (int s = tid; s < k; s += T) sm[s] = add(sm[s], sm[s + k]);
+        __syncthreads();
+    }
+    if (tid < 32) {
+        constexpr int W = BS < 32 ? BS : 32;
+        double r = tid < W ? sm[tid] : 0.0;
+        for (int off = W / 2; off >= 1; off >>= 1) r = add(r, __shfl_down_sync(0xffffffffu, r, off));
+        if (tid == 0) {
+            *A.result = r;
+            *A.ticket = 0u;
+        }
+    }
+}
+
 // ---- generic path (block_size > 1024): lattice in global memory ----------
 template <int MODE>
 __global__ void __launch_bounds__(256) k_lattice_global(RArgs A) {
@@ -227,6 +377,15 @@ __global__ void __launch_bounds__(1024) k_final_generic(RArgs A) {
     if (threadIdx.x == 0) *A.result = v;
 }
 
+// SB200_NO_TMA=1 selects the register-unrolled lattice kernel (A/B checks).
+static bool use_tma() {
+    static const bool on = [] {
+        const char *e = getenv("SB200_NO_TMA");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 template <int MODE>
 static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
     clear_error();
@@ -248,6 +407,22 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
     // thread while staying under 64 registers (4 CTAs of 256 per SM).
     constexpr int UN = 16, UD = 8, UF = 4;
     constexpr int U = MODE == R_NORM ? UN : (MODE == R_DOT ? UD : UF);
+    // TMA ring: ~32 KB of stages per CTA (so <= 4 CTAs/SM by shared memory)
+    constexpr int NA = NArr<MODE>::v;
+    const bool tma_ok = aligned16(A.u) && aligned16(A.v) && (MODE != R_FUSED || (aligned16(A.x) && aligned16(A.r)));
+    if (tma_ok && use_tma() && (A.bs == 64 || A.bs == 128 || A.bs == 256 || A.bs == 512)) {
+#define SB_TMA(T_, SPT_)                                                                        \
+    k_lattice_tma<T_, SPT_, MODE, (32768 / (NA * T_ * SPT_ * 8) > 16 ? 16 : 32768 / (NA * T_ * SPT_ * 8))> \
+        <<<grid, T_ + 32, 0, st>>>(A)
+        switch (A.bs) {
+            case 64: SB_TMA(64, 1); break;
+            case 128: SB_TMA(128, 1); break;
+            case 256: SB_TMA(256, 1); break;
+            default: SB_TMA(256, 2); break;
+        }
+#undef SB_TMA
+        return launch_check(name);
+    }
 #define SB_LAT(T_, SPT_) k_lattice<T_, SPT_, MODE, U><<<grid, T_, 0, st>>>(A)
     switch (A.bs) {
         case 2: SB_LAT(2, 1); break;

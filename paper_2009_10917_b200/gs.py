@@ -26,10 +26,18 @@ def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) ->
     seed rows [0, len(carry)) instead of +0.0 (multi-GPU carry halo)."""
     dev = q_local.device
     L = _lib.lib()
+    ncarry = 0 if carry is None else int(carry.shape[0])
+    plan = op.plan() if hasattr(op, "plan") else None
+    if plan is not None:
+        _lib.check(L.sb_bs6_gather_planned(plan.data_ptr(), op.n_blocks, op.nodes_per_block,
+                                           op.row_starts.data_ptr(), op.col_ids.data_ptr(), op.ng,
+                                           op.nl, q_local.data_ptr(), out.data_ptr(),
+                                           None if carry is None else carry.data_ptr(), ncarry,
+                                           _lib.stream_handle(dev)), "bs6_gather")
+        return out
     bst = _dev_int(op.block_starts, "block_starts", dev)
     rs = _dev_int(op.row_starts, "row_starts", dev)
     ci = _dev_int(op.col_ids, "col_ids", dev)
-    ncarry = 0 if carry is None else int(carry.shape[0])
     _lib.check(L.sb_bs6_gather(bst.data_ptr(), int(bst.shape[0]) - 1, rs.data_ptr(), ci.data_ptr(),
                                op.ng, int(ci.shape[0]), op.nodes_per_block, q_local.data_ptr(),
                                out.data_ptr(), None if carry is None else carry.data_ptr(), ncarry,

@@ -14,6 +14,7 @@ reference's greedy rule in both cases (sb_build_block_starts).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from functools import cached_property
 
@@ -102,6 +103,27 @@ class GatherOp:
     @property
     def n_blocks(self) -> int:
         return int(self.block_starts.shape[0]) - 1
+
+    def plan(self) -> torch.Tensor | None:
+        """Super-block plan for the pipelined BS6 kernel (sb_bs6_make_plan),
+        built once per operator; None when the operator does not qualify."""
+        p = self.__dict__.get("_plan", False)
+        if p is not False:
+            return p
+        p = None
+        if (self.row_starts.is_cuda and self.col_ids.is_cuda and self.block_starts.is_cuda
+                and self.row_starts.data_ptr() % 16 == 0 and self.col_ids.data_ptr() % 16 == 0
+                and os.environ.get("SB200_NO_PIPE") != "1"):
+            L = _lib.lib()
+            size = int(L.sb_bs6_plan_size(self.n_blocks, self.nodes_per_block))
+            if size > 0:
+                dev = self.row_starts.device
+                p = torch.empty(size, dtype=torch.int32, device=dev)
+                _lib.check(L.sb_bs6_make_plan(self.block_starts.data_ptr(), self.n_blocks,
+                                              self.row_starts.data_ptr(), self.nodes_per_block,
+                                              p.data_ptr(), _lib.stream_handle(dev)), "bs6 plan")
+        object.__setattr__(self, "_plan", p)
+        return p
 
 
 def build_mesh(K: int, p: int, device=None) -> MeshConnectivity:

@@ -192,3 +192,24 @@ def test_reference_numpy_operator_drop_in(sb, golden):
     out = sb.bs6_gather(op, q)
     assert isinstance(out, np.ndarray)
     assert np.array_equal(out, arr[f"bs6_{tag}"])
+
+
+@pytest.mark.parametrize("K,p,npb", [(20, 7, 512), (13, 2, 16), (7, 15, 2048), (25, 1, 64), (3, 3, 8)])
+def test_pipelined_bs6_matches_unplanned(sb, K, p, npb):
+    """sb_bs6_gather_planned (persistent, cp.async pipeline) == sb_bs6_gather, with carry."""
+    import types
+    from paper_2009_10917_b200.gs import bs6_gather_into
+    mesh = sb.build_mesh(K, p)
+    op = sb.build_gather(mesh, npb)
+    assert op.plan() is not None
+    plain = types.SimpleNamespace(ng=op.ng, nl=op.nl, row_starts=op.row_starts, col_ids=op.col_ids,
+                                  block_starts=op.block_starts, nodes_per_block=npb,
+                                  n_blocks=op.n_blocks)
+    q = d(np.random.default_rng([K, p, npb]).uniform(-1, 1, mesh.nl))
+    carry = d(np.random.default_rng(1).uniform(-1, 1, min(mesh.ng, 1000)))
+    for c in (None, carry):
+        a = torch.empty(mesh.ng, dtype=torch.float64, device="cuda")
+        b = torch.empty_like(a)
+        bs6_gather_into(op, q, a, c)
+        bs6_gather_into(plain, q, b, c)
+        assert torch.equal(a, b)

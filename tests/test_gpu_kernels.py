@@ -230,3 +230,42 @@ def test_large_n_bitwise_vs_oracle(sb, oracle, n):
         assert np.array_equal(h(yy), ye)
     finally:
         oracle.set_threads(1)
+
+
+def test_fallback_kernels_match(sb):
+    """The register-unrolled lattice and one-tile-per-CTA gather/scatter kernels
+    (SB200_NO_TMA / SB200_NO_PIPE) must agree bitwise with the fast paths."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, ".")
+import paper_2009_10917_b200 as sb
+from paper_2009_10917_b200 import kernels as K
+g = torch.Generator(device="cuda"); g.manual_seed(5)
+out = []
+for n in (0, 7, 131073, 3_000_017):
+    x = torch.empty(n, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g)
+    y = torch.empty(n, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g)
+    for cfg in (sb.ReductionConfig(), sb.ReductionConfig(64, 37), sb.ReductionConfig(512, 100)):
+        out.append(sb.bs3_norm2(x, cfg).hex()); out.append(sb.bs4_dot(x, y, cfg).hex())
+        xx, rr = x.clone(), y.clone()
+        out.append(sb.bs5_fused_cg_update(0.3, y, x, xx, rr, cfg).hex())
+        out.append(float(xx.sum()).hex() + float(rr.sum()).hex())
+m = sb.build_mesh(9, 5); ids = sb.build_scatter_ids(m, mask={0, 17, 99})
+qg = torch.empty(m.ng, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g)
+ql = torch.zeros(m.nl, dtype=torch.float64, device="cuda")
+sb.bs7_scatter(ids, qg, ql); out.append(float(ql.sum()).hex())
+ids2 = sb.build_scatter_ids(m); sb.bs7_scatter(ids2, qg, ql); out.append(float((ql * ql).sum()).hex())
+print(" ".join(out))
+'''
+    res = []
+    for env_extra in ({}, {"SB200_NO_TMA": "1", "SB200_NO_PIPE": "1"}):
+        env = dict(os.environ, **env_extra)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(r.stdout.strip())
+    assert res[0] == res[1]
