@@ -155,37 +155,60 @@ def cpu_model():
 
 # ------------------------------------------------------------ CPU (oracle)
 
-def run_cpu_sample(seconds: float, K: int, order: int, bs: int, nb: int):
-    """Time the oracle port (the reference algorithm in C, all host threads)
-    on a bounded sample of the workload: BS1-BS5 at n_cpu, BS6/BS7 at K_cpu."""
+def run_cpu_sample(seconds: float, K: int, order: int, bs: int, nb: int, port: str = "numpy"):
+    """Time a CPU port of the reference hot path on all host threads over a
+    bounded sample of the workload (BS1-BS5 at n_cpu, BS6/BS7 at K_cpu):
+      port="numpy": oracle/np_port.py -- the reference's own implementation
+                    strategy (numpy temporaries over thread-pool spans);
+      port="c":     oracle/sb_oracle.c -- the same algorithm in C + OpenMP."""
     import numpy as np
 
     from oracle import oracle as O
+    from paper_2009_10917_b200.core import bytes_moved
 
     threads = cpu_cores()
     O.set_threads(threads)
-    n = 20_000_000
-    Kc = max(2, min(K, 33))
+    n = 20_000_000 if port == "c" else 10_000_000
+    Kc = max(2, min(K, 33 if port == "c" else 24))
     rng = np.random.default_rng([0, n])
     x, y, p, ap = (rng.uniform(-1, 1, n) for _ in range(4))
     l2g = O.build_mesh(Kc, order)
     ng = (Kc * order + 1) ** 3
-    rs, ci, _ = O.build_gather(l2g, ng, 512)
+    rs, ci, bst = O.build_gather(l2g, ng, 512)
     ids = O.build_scatter_ids(l2g, ng)
     q = rng.uniform(-1, 1, l2g.shape[0])
     qg = rng.uniform(-1, 1, ng)
     ql = np.zeros(l2g.shape[0])
-    from paper_2009_10917_b200.core import bytes_moved
     nl = l2g.shape[0]
-    fns = {
-        "bs1": (lambda: O.bs1_copy(x, y), bytes_moved("bs1", n=n)),
-        "bs2": (lambda: O.bs2_axpy(0.5, x, -0.25, y), bytes_moved("bs2", n=n)),
-        "bs3": (lambda: O.bs3_norm2(x, bs, nb), bytes_moved("bs3", n=n)),
-        "bs4": (lambda: O.bs4_dot(x, y, bs, nb), bytes_moved("bs4", n=n)),
-        "bs5": (lambda: O.bs5_fused_cg_update(0.1, p, ap, x, y, bs, nb), bytes_moved("bs5", n=n)),
-        "bs6": (lambda: O.bs6_gather(rs, ci, q), bytes_moved("bs6", nl=nl, ng=ng)),
-        "bs7": (lambda: O.bs7_scatter(ids, qg, ql), bytes_moved("bs7", nl=nl, ng=ng)),
-    }
+    pool = None
+    if port == "c":
+        calls = {
+            "bs1": lambda: O.bs1_copy(x, y),
+            "bs2": lambda: O.bs2_axpy(0.5, x, -0.25, y),
+            "bs3": lambda: O.bs3_norm2(x, bs, nb),
+            "bs4": lambda: O.bs4_dot(x, y, bs, nb),
+            "bs5": lambda: O.bs5_fused_cg_update(0.1, p, ap, x, y, bs, nb),
+            "bs6": lambda: O.bs6_gather(rs, ci, q),
+            "bs7": lambda: O.bs7_scatter(ids, qg, ql),
+        }
+        impl = f"oracle/sb_oracle.c (C -O2, OpenMP, {threads} threads)"
+    else:
+        from oracle import np_port as NP
+        pool = NP.Pool(threads)
+        calls = {
+            "bs1": lambda: NP.bs1_copy(pool, x, y),
+            "bs2": lambda: NP.bs2_axpy(pool, 0.5, x, -0.25, y),
+            "bs3": lambda: NP.reduce_product(pool, x, x, bs, nb),
+            "bs4": lambda: NP.reduce_product(pool, x, y, bs, nb),
+            "bs5": lambda: NP.bs5_fused_cg_update(pool, 0.1, p, ap, x, y, bs, nb),
+            "bs6": lambda: NP.bs6_gather(pool, rs, ci, bst, q),
+            "bs7": lambda: NP.bs7_scatter(pool, ids, qg, ql),
+        }
+        impl = f"oracle/np_port.py (numpy, thread pool of {threads})"
+    byts = {t: bytes_moved(t, n=n) for t in TESTS[:5]}
+    byts["bs6"] = bytes_moved("bs6", nl=nl, ng=ng)
+    byts["bs7"] = bytes_moved("bs7", nl=nl, ng=ng)
+    fns = {t: (calls[t], byts[t]) for t in TESTS}
     for f, _ in fns.values():  # warm
         f()
     per = {}
@@ -205,8 +228,10 @@ def run_cpu_sample(seconds: float, K: int, order: int, bs: int, nb: int):
             tot_t += dt
         if time.perf_counter() - t_start > seconds:
             break
-    sample = (f"oracle port (C, -O2, {threads} threads) on {cpu_model()}: {reps} passes of "
-              f"BS1-BS5 at n={n:.0e} and BS6/BS7 at K={Kc}, N={order} (NL={nl}, NG={ng})")
+    if pool is not None:
+        pool.close()
+    sample = (f"{impl} on {cpu_model()}: {reps} passes of BS1-BS5 at n={n:.0e} and BS6/BS7 "
+              f"at K={Kc}, N={order} (NL={nl}, NG={ng}); GB/s = sum(bytes_moved) / sum(time)")
     per_gbs = {k: v[1] / v[0] / 1e9 for k, v in per.items()}
     return tot_b / tot_t / 1e9, threads, sample, per_gbs
 
@@ -246,7 +271,10 @@ class Workload:
             nl, ng = self.slab.nl, self.slab.ng_owned
             self.mesh_desc = dist_ctx.mesh_desc
         self.q = vec(nl)
-        self.qg = vec(ng if dist_ctx is None else self.slab.ng_local_read)
+        if dist_ctx is None:
+            self.qg = vec(ng)
+        else:  # BS7 reads the rank's q_global window (own rows + halo plane)
+            dist_ctx.scat.window.uniform_(-1, 1, generator=gen)
         self.ql = torch.zeros(nl, dtype=torch.float64, device=device)
         self.gout = torch.empty(ng, dtype=torch.float64, device=device)
         _ = self.ids.has_mask if dist_ctx is None else None
@@ -345,7 +373,7 @@ def run_e2e(args, device, steps):
     qg = hvec(mesh.ng)
     ql = torch.zeros(mesh.nl, dtype=torch.float64).pin_memory()
     nb8 = 8 * n
-    h2d = {"bs1": 2 * nb8, "bs2": 2 * nb8, "bs3": nb8, "bs4": 2 * nb8, "bs5": 4 * nb8,
+    h2d = {"bs1": nb8, "bs2": 2 * nb8, "bs3": nb8, "bs4": 2 * nb8, "bs5": 4 * nb8,
            "bs6": 8 * mesh.nl, "bs7": 8 * mesh.ng + 8 * mesh.nl}
     d2h = {"bs1": nb8, "bs2": nb8, "bs3": 8, "bs4": 8, "bs5": 2 * nb8 + 8, "bs6": 8 * mesh.ng,
            "bs7": 8 * mesh.nl}
@@ -464,10 +492,16 @@ def main_ours(args):
             result["e2e"] = run_e2e(args, device, args.e2e_steps)
         if not args.no_cpu_baseline:
             v, cores, sample, per = run_cpu_sample(args.cpu_seconds, args.K, args.order,
-                                                   args.block_size, args.n_blocks)
-            result["cpu_baseline"] = {"value": round(v, 3), "unit": "GB/s", "cores": cores,
-                                      "kind": "port", "sample": sample,
-                                      "per_test": {k: round(x, 3) for k, x in per.items()}}
+                                                   args.block_size, args.n_blocks, "numpy")
+            vc, _, sample_c, per_c = run_cpu_sample(args.cpu_seconds / 2, args.K, args.order,
+                                                    args.block_size, args.n_blocks, "c")
+            result["cpu_baseline"] = {
+                "value": round(v, 3), "unit": "GB/s", "cores": cores, "kind": "port",
+                "sample": sample, "per_test": {k: round(x, 3) for k, x in per.items()},
+                "c_port": {"value": round(vc, 3), "sample": sample_c,
+                           "per_test": {k: round(x, 3) for k, x in per_c.items()},
+                           "note": "same algorithm restated in C + OpenMP (stronger than "
+                                   "the reference's numpy implementation)"}}
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -481,12 +515,11 @@ def main_reference(args):
     t0 = time.perf_counter()
     vals = []
     sample = cores = per = None
-    for _ in range(max(1, args.warmup)):
-        run_cpu_sample(min(2.0, args.cpu_seconds), args.K, args.order, args.block_size,
-                       args.n_blocks)
+    run_cpu_sample(0.0, args.K, args.order, args.block_size, args.n_blocks, "numpy")  # warm
     for _ in range(args.steps):
-        v, cores, sample, per = run_cpu_sample(max(1.0, args.cpu_seconds / max(1, args.steps)),
-                                               args.K, args.order, args.block_size, args.n_blocks)
+        v, cores, sample, per = run_cpu_sample(max(0.5, args.cpu_seconds / max(1, args.steps)),
+                                               args.K, args.order, args.block_size, args.n_blocks,
+                                               "numpy")
         vals.append(v)
     value = statistics.median(vals)
     out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",

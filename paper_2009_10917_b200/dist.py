@@ -1,0 +1,317 @@
+"""Multi-GPU BS1-BS7: slab partition + NCCL exchanges (one process per GPU).
+
+New capability relative to the reference (which is single-process; SURVEY
+§2.2, §8e): the seven streaming tests across the GPUs of one node, launched
+by torchrun with torch.distributed over NCCL.
+
+Vectors (BS1-BS5): contiguous chunks, the reference's span split
+(parallel.py:43-53) with exactly one span per rank.  BS1/BS2 need no
+communication.  BS3/BS4/BS5 reduce the local chunk on the rank's lattice
+(same ReductionConfig), all-gather the one-double partials (NCCL) and sum
+them in rank order from +0.0 on the device (sb_sum_ordered): deterministic
+for a fixed world size and identical on every rank; <= 1e-12 relative to the
+exact sum like the reference's own tolerance (test_kernels.py:135-139).  It
+is not bitwise the 1-GPU lattice (that would serialise the slot chains).
+
+Mesh (BS6/BS7): z-slabs of element layers, layer counts by the same span
+split (K=143 over 8 ranks -> 18,...,18,17).  Rank r owns the global rows of
+planes [z0*p, z1*p) (the last rank also the top plane z1*p).
+  BS6, bitwise equal to the 1-GPU gather: every element of rank r has a
+  smaller element id -- hence smaller local index -- than every element of
+  rank r+1, so an interface row's ascending sum is (rank r's terms) then
+  (rank r+1's terms).  Rank r gathers the partial sums of its top plane and
+  sends them to r+1 ("carry"), which seeds those rows' accumulators with them
+  (sb_bs6_gather* carry_in) and continues in order.
+  BS7: rank r needs q_global of its top plane, owned by r+1: a one-plane halo
+  sent from r+1 to r before the scatter.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .parallel import split_range
+
+
+# ---------------------------------------------------------------- partitions
+
+def rank_span(n: int, world: int, rank: int) -> tuple[int, int]:
+    """parallel.py:43-53 with exactly `world` (possibly empty) contiguous spans."""
+    step, extra = divmod(n, world)
+    lo = rank * step + min(rank, extra)
+    return lo, lo + step + (1 if rank < extra else 0)
+
+
+@dataclass(frozen=True)
+class SlabPartition:
+    """z-slab partition of the K^3 order-p mesh over `world` ranks."""
+
+    K: int
+    p: int
+    world: int
+
+    def __post_init__(self):
+        if self.world < 1 or self.world > self.K:
+            raise ValueError(f"need 1 <= world <= K, got world={self.world}, K={self.K}")
+
+    @property
+    def g(self) -> int:
+        return self.K * self.p + 1
+
+    @property
+    def plane(self) -> int:
+        """Rows (global DOFs) per lattice plane."""
+        return self.g * self.g
+
+    @property
+    def npe3(self) -> int:
+        return (self.p + 1) ** 3
+
+    def layers(self, rank: int) -> tuple[int, int]:
+        spans = split_range(self.K, self.world)
+        return spans[rank]
+
+    def own_planes(self, rank: int) -> tuple[int, int]:
+        z0, z1 = self.layers(rank)
+        top = z1 * self.p + (1 if rank == self.world - 1 else 0)
+        return z0 * self.p, top
+
+    def send_plane(self, rank: int):
+        """Plane whose partials rank sends up (None for the last rank)."""
+        return None if rank == self.world - 1 else self.layers(rank)[1] * self.p
+
+    def nl(self, rank: int) -> int:
+        z0, z1 = self.layers(rank)
+        return self.K * self.K * (z1 - z0) * self.npe3
+
+    def local_span(self, rank: int) -> tuple[int, int]:
+        """This rank's slice of the global element-local vector."""
+        z0, z1 = self.layers(rank)
+        base = self.K * self.K * self.npe3
+        return z0 * base, z1 * base
+
+    def row_span(self, rank: int) -> tuple[int, int]:
+        """Global rows (DOFs) this rank owns (its slice of the gathered vector)."""
+        c0, c1 = self.own_planes(rank)
+        return c0 * self.plane, c1 * self.plane
+
+    def ng_own(self, rank: int) -> int:
+        a, b = self.row_span(rank)
+        return b - a
+
+    def read_span(self, rank: int) -> tuple[int, int]:
+        """Global rows BS7 reads: own planes plus the top interface plane (halo)."""
+        z0, z1 = self.layers(rank)
+        return z0 * self.p * self.plane, (z1 * self.p + 1) * self.plane
+
+
+# ------------------------------------------------------------- reductions
+
+class DistReducer:
+    """All-gather of per-rank lattice scalars + device rank-order sum."""
+
+    def __init__(self, world: int, device, group=None, sum_fn=None):
+        self.world, self.device, self.group = world, torch.device(device), group
+        self.buf = torch.empty(world, dtype=torch.float64, device=self.device)
+        self.sum_fn = sum_fn or _gpu_sum_ordered
+
+    def combine(self, local: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        if self.buf.is_cuda:
+            dist.all_gather_into_tensor(self.buf, local.reshape(1), group=self.group)
+        else:  # gloo has no all_gather_into_tensor
+            parts = list(self.buf.split(1))
+            dist.all_gather(parts, local.reshape(1).clone(), group=self.group)
+        res = out if out is not None else torch.empty(1, dtype=torch.float64, device=self.device)
+        self.sum_fn(self.buf, res)
+        return res
+
+
+def _gpu_sum_ordered(values: torch.Tensor, res: torch.Tensor) -> None:
+    L = _lib.lib()
+    _lib.check(L.sb_sum_ordered(values.data_ptr(), values.shape[0], res.data_ptr(),
+                                _lib.stream_handle(values.device)), "sum_ordered")
+
+
+def combine_host(values) -> float:
+    """Reference semantics of DistReducer.combine: ((0.0 + v0) + v1) + ..."""
+    acc = 0.0
+    for v in values:
+        acc = acc + float(v)
+    return acc
+
+
+# -------------------------------------------------------------- BS6 / BS7
+
+def _gpu_gather(op, q, out, carry):
+    from .gs import bs6_gather_into
+    return bs6_gather_into(op, q, out, carry)
+
+
+class DistGather:
+    """BS6 over a z-slab with the one-way carry halo (bitwise the 1-GPU result).
+
+    own_op: rows of own_planes(rank) over the slab's local DOFs;
+    send_op: rows of send_plane(rank) over the same DOFs (None on the last rank).
+    gather_fn(op, q, out, carry) runs one CSR gather (libsb200 by default).
+    """
+
+    def __init__(self, part: SlabPartition, rank: int, own_op, send_op, device,
+                 gather_fn=_gpu_gather, group=None):
+        self.part, self.rank, self.own_op, self.send_op = part, rank, own_op, send_op
+        self.device, self.gather_fn, self.group = torch.device(device), gather_fn, group
+        plane = part.plane
+        self.send_buf = torch.empty(plane, dtype=torch.float64, device=self.device) \
+            if send_op is not None else None
+        self.carry = torch.empty(plane, dtype=torch.float64, device=self.device) if rank > 0 else None
+
+    @classmethod
+    def build(cls, part: SlabPartition, rank: int, device, nodes_per_block: int = 512, group=None):
+        from .mesh import build_slab_gather
+        z0, z1 = part.layers(rank)
+        c0, c1 = part.own_planes(rank)
+        own = build_slab_gather(part.K, part.p, z0, z1, c0, c1, nodes_per_block, device)
+        sp = part.send_plane(rank)
+        send = None if sp is None else build_slab_gather(part.K, part.p, z0, z1, sp, sp + 1,
+                                                         nodes_per_block, device)
+        return cls(part, rank, own, send, device, group=group)
+
+    def exchange(self) -> None:
+        ops = []
+        if self.send_buf is not None:
+            ops.append(dist.P2POp(dist.isend, self.send_buf, self.rank + 1, group=self.group))
+        if self.carry is not None:
+            ops.append(dist.P2POp(dist.irecv, self.carry, self.rank - 1, group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def gather(self, q_slab: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """out (= this rank's rows of the global gathered vector) from q_slab."""
+        if self.send_op is not None:
+            self.gather_fn(self.send_op, q_slab, self.send_buf, None)
+        self.exchange()
+        self.gather_fn(self.own_op, q_slab, out, self.carry)
+        return out
+
+
+class DistScatter:
+    """BS7 over a z-slab: q_local[n] = q_global[l2g[n]] with a one-plane halo."""
+
+    def __init__(self, part: SlabPartition, rank: int, ids_local: torch.Tensor, device, group=None,
+                 scatter_fn=None):
+        self.part, self.rank, self.device, self.group = part, rank, torch.device(device), group
+        self.ids = ids_local  # ids relative to read_span(rank)[0]
+        self.scatter_fn = scatter_fn or _gpu_scatter
+        a, b = part.read_span(rank)
+        self.window = torch.empty(b - a, dtype=torch.float64, device=self.device)
+        self.own_rows = part.ng_own(rank) if rank < part.world - 1 else b - a
+
+    @classmethod
+    def build(cls, part: SlabPartition, rank: int, device, group=None):
+        from .mesh import build_slab_l2g
+        z0, z1 = part.layers(rank)
+        l2g = build_slab_l2g(part.K, part.p, z0, z1, device)
+        l2g -= part.read_span(rank)[0]
+        return cls(part, rank, l2g, device, group=group)
+
+    def exchange(self) -> None:
+        """Send my bottom plane down to rank-1, receive my top plane from rank+1."""
+        plane = self.part.plane
+        ops = []
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.isend, self.window[:plane], self.rank - 1, group=self.group))
+        if self.rank < self.part.world - 1:
+            ops.append(dist.P2POp(dist.irecv, self.window[self.own_rows:], self.rank + 1,
+                                  group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def scatter(self, q_local: torch.Tensor) -> None:
+        """window[:own_rows] must hold this rank's q_global rows."""
+        self.exchange()
+        self.scatter_fn(self.ids, self.window, q_local)
+
+
+def _gpu_scatter(ids: torch.Tensor, window: torch.Tensor, q_local: torch.Tensor) -> None:
+    from .gs import bs7_scatter
+    bs7_scatter(_Ids(ids), window, q_local)
+
+
+class _Ids:
+    """ScatterIds view over a device id tensor (unmasked, ids >= 0 by construction)."""
+
+    def __init__(self, ids):
+        self.ids = ids
+        self.has_mask = False
+        self.max_id = -1  # range guaranteed by construction (read_span)
+
+    @property
+    def nl(self):
+        return int(self.ids.shape[0])
+
+
+# -------------------------------------------------------------- bench glue
+
+class BenchContext:
+    """Per-rank state of bench.py's weak-scaling step (n per rank, K_g^3 mesh)."""
+
+    def __init__(self, rank: int, world: int, args, device):
+        self.rank, self.world, self.device = rank, world, torch.device(device)
+        self.reducer = DistReducer(world, device)
+        Kg = max(world, int(round(args.K * world ** (1.0 / 3.0))))
+        self.part = SlabPartition(Kg, args.order, world)
+        g = self.part.g
+        self.mesh_desc = {"K_global": Kg, "order": args.order, "ng_global": g ** 3,
+                          "nl_global": Kg ** 3 * (args.order + 1) ** 3,
+                          "slab_layers": [self.part.layers(r) for r in range(world)],
+                          "partition": "z-slabs, carry halo (BS6), one-plane halo (BS7)"}
+        # per step: 7 kernels + (3 reductions x (NCCL all-gather + ordered sum)) + BS6 send-plane
+        # gather + NCCL carry + BS7 NCCL halo
+        self.launches_per_step = 7 + 3 * 1 + 1
+
+    def build_slab(self, K, order, device):
+        self.gather = DistGather.build(self.part, self.rank, device)
+        self.scat = DistScatter.build(self.part, self.rank, device)
+        return _SlabInfo(self.part, self.rank)
+
+    def call(self, w, test):
+        from . import kernels as KN
+        if test == "bs1":
+            w.sb.bs1_copy(w.x, w.y)
+        elif test == "bs2":
+            w.sb.bs2_axpy(0.5, w.x, -0.25, w.y)
+        elif test == "bs3":
+            self.reducer.combine(KN.bs3_norm2_async(w.x, w.cfg, out=w.res), out=w.res)
+        elif test == "bs4":
+            self.reducer.combine(KN.bs4_dot_async(w.x, w.y, w.cfg, out=w.res), out=w.res)
+        elif test == "bs5":
+            self.reducer.combine(KN.bs5_fused_cg_update_async(1e-3, w.p, w.ap, w.x, w.r, w.cfg,
+                                                              out=w.res), out=w.res)
+        elif test == "bs6":
+            self.gather.gather(w.q, w.gout)
+        else:
+            self.scat.scatter(w.ql)
+
+
+@dataclass
+class _SlabInfo:
+    part: SlabPartition
+    rank: int
+
+    @property
+    def nl(self):
+        return self.part.nl(self.rank)
+
+    @property
+    def ng_owned(self):
+        return self.part.ng_own(self.rank)
+
+    @property
+    def ng_local_read(self):
+        a, b = self.part.read_span(self.rank)
+        return b - a

@@ -12,7 +12,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, hoststream
 
 
 def _dev_int(a, name, device):
@@ -45,19 +45,97 @@ def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) ->
     return out
 
 
+def _prefix_need(idx: torch.Tensor, ends) -> list[int]:
+    """need[j] = 1 + max(idx[:ends[j]]) (the input prefix a chunk may touch)."""
+    pm = torch.cummax(idx.to(torch.int64), 0).values
+    e = torch.as_tensor([max(int(v), 1) - 1 for v in ends], dtype=torch.int64, device=idx.device)
+    return [int(v) + 1 for v in pm[e].tolist()]
+
+
+def _bs6_host_jobs(op):
+    """Row chunks of ~CHUNK rows on block boundaries + the q prefix each needs (cached)."""
+    jobs = op.__dict__.get("_host_jobs")
+    if jobs is None:
+        bst = op.block_starts.cpu().numpy()
+        cuts = [0]
+        for b in range(1, bst.shape[0]):
+            if bst[b] - bst[cuts[-1]] >= hoststream.CHUNK or b == bst.shape[0] - 1:
+                cuts.append(b)
+        rows = [int(bst[c]) for c in cuts]
+        ends = op.row_starts[torch.as_tensor(rows[1:], device=op.row_starts.device)].tolist()
+        need = _prefix_need(op.col_ids, ends)
+        jobs = [(rows[i], rows[i + 1], need[i], cuts[i], cuts[i + 1]) for i in range(len(cuts) - 1)]
+        object.__setattr__(op, "_host_jobs", jobs)
+    return jobs
+
+
+def _bs6_host(op, q_local):
+    """Host q_local -> host result, upload / row-chunk gathers / download overlapped."""
+    hq = hoststream.as_host_tensor(q_local, "q_local")
+    dev = op.row_starts.device
+    L = _lib.lib()
+    qd = torch.empty(op.nl, dtype=torch.float64, device=dev)
+    outd = torch.empty(op.ng, dtype=torch.float64, device=dev)
+    # a fresh result like the reference (gs.py:20), page-locked (torch's caching
+    # host allocator): full-speed D2H without first-touch page faults
+    res = torch.empty(op.ng, dtype=torch.float64, pin_memory=True)
+    jobs = _bs6_host_jobs(op)
+    blocks = {j[0]: (j[3], j[4]) for j in jobs}
+
+    def launch(r_lo, r_hi):
+        b_lo, b_hi = blocks[r_lo]
+        _lib.check(L.sb_bs6_gather(op.block_starts.data_ptr() + 4 * b_lo, b_hi - b_lo,
+                                   op.row_starts.data_ptr(), op.col_ids.data_ptr(), op.ng, op.nl,
+                                   op.nodes_per_block, qd.data_ptr(), outd.data_ptr(), None, 0,
+                                   _lib.stream_handle(dev)), "bs6_gather")
+
+    hoststream.run_prefix(hq, qd, outd, res, [j[:3] for j in jobs], launch, dev)
+    return res.numpy() if isinstance(q_local, np.ndarray) else res
+
+
 def bs6_gather(op, q_local, out=None):
     """gs.py:10-39: out[r] = sum of q_local over row r's columns, ascending order."""
     if q_local.shape[0] != op.nl:
         raise ValueError(f"local vector length {q_local.shape[0]} != operator NL {op.nl}")
     host = not (isinstance(q_local, torch.Tensor) and q_local.is_cuda)
+    if host and out is None and isinstance(op.row_starts, torch.Tensor) and op.row_starts.is_cuda:
+        return _bs6_host(op, q_local)
     q = _lib.stage(q_local, torch.float64, "q_local").dev
     if out is None:
         out = torch.empty(op.ng, dtype=torch.float64, device=q.device)
     bs6_gather_into(op, q, out)
     if host:
-        res = out.cpu()
+        # a fresh result like the reference (gs.py:20), in page-locked memory from
+        # torch's caching host allocator: full-speed D2H, no first-touch faults
+        res = torch.empty(op.ng, dtype=torch.float64, pin_memory=True)
+        res.copy_(out, non_blocking=True)
+        torch.cuda.current_stream(q.device).synchronize()
         return res.numpy() if isinstance(q_local, np.ndarray) else res
     return out
+
+
+def _bs7_host(ids, q_global, q_local) -> None:
+    """Unmasked scatter between host vectors: q_global upload, local-chunk scatters
+    and q_local download overlapped (q_local is write-only, never uploaded)."""
+    hg = hoststream.as_host_tensor(q_global, "q_global")
+    hl = hoststream.as_host_tensor(q_local, "q_local")
+    dev = ids.ids.device
+    nl, ng = ids.nl, int(hg.shape[0])
+    jobs = ids.__dict__.get("_host_jobs")
+    if jobs is None:
+        cuts = list(range(0, nl, hoststream.CHUNK)) + [nl]
+        need = _prefix_need(ids.ids, cuts[1:])
+        jobs = [(cuts[i], cuts[i + 1], need[i]) for i in range(len(cuts) - 1)]
+        ids.__dict__["_host_jobs"] = jobs
+    L = _lib.lib()
+    gd = torch.empty(ng, dtype=torch.float64, device=dev)
+    ld = torch.empty(nl, dtype=torch.float64, device=dev)
+
+    def launch(lo, hi):
+        _lib.check(L.sb_bs7_scatter(ids.ids.data_ptr() + 4 * lo, hi - lo, gd.data_ptr(), ng,
+                                    ld.data_ptr() + 8 * lo, 0, _lib.stream_handle(dev)), "bs7_scatter")
+
+    hoststream.run_prefix(hg, gd, ld, hl, jobs, launch, dev)
 
 
 def bs7_scatter(ids, q_global, q_local) -> None:
@@ -70,9 +148,21 @@ def bs7_scatter(ids, q_global, q_local) -> None:
         max_id = int(np.max(ids.ids)) if ids.ids.size else -1
     if ids.nl and max_id >= ng:
         raise ValueError(f"scatter id {max_id} out of range [0, {ng})")
+    if (hoststream.all_host(q_global, q_local) and not ids.has_mask
+            and isinstance(ids.ids, torch.Tensor) and ids.ids.is_cuda and ids.ids.data_ptr() % 16 == 0):
+        _bs7_host(ids, q_global, q_local)
+        return
     sg = _lib.stage(q_global, torch.float64, "q_global")
     dev = sg.dev.device
-    sl = _lib.stage(q_local, torch.float64, "q_local", dev)
+    if not ids.has_mask and not (isinstance(q_local, torch.Tensor) and q_local.is_cuda):
+        # every entry is overwritten: the host q_local is download-only
+        host = q_local if isinstance(q_local, torch.Tensor) else np.asarray(q_local)
+        if host.dtype not in (np.float64, torch.float64):
+            raise TypeError(f"q_local: expected float64, got {host.dtype}")
+        sl = _lib.Staged(torch.empty(ids.nl, dtype=torch.float64, device=dev), host,
+                         "cpu" if isinstance(host, torch.Tensor) else "numpy")
+    else:
+        sl = _lib.stage(q_local, torch.float64, "q_local", dev)
     id_t = _dev_int(ids.ids, "ids", dev)
     L = _lib.lib()
     _lib.check(L.sb_bs7_scatter(id_t.data_ptr(), int(id_t.shape[0]), sg.dev.data_ptr(), ng,

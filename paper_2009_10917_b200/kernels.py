@@ -22,7 +22,7 @@ from dataclasses import dataclass
 
 import torch
 
-from . import _lib
+from . import _lib, hoststream
 from .core import DVector, check_same_length
 
 
@@ -100,6 +100,11 @@ def bs1_copy(x, y) -> None:
         _lib.check(L.sb_bs1_copy(x.data_ptr(), y.data_ptr(), x.shape[0], _lib.stream_handle(dev)),
                    "bs1_copy")
         return
+    if hoststream.all_host(x, y):
+        hx, hy = hoststream.as_host_tensor(x, "x"), hoststream.as_host_tensor(y, "y")
+        hoststream.run(hx.shape[0], {"x": hx}, {"y": hy}, ("y",),
+                       lambda d, lo, hi: bs1_copy(d["x"][lo:hi], d["y"][lo:hi]))
+        return
     sx, sy = _stage_all(("x", "y"), (x, y))
     bs1_copy(sx.dev, sy.dev)
     sy.writeback()
@@ -116,6 +121,11 @@ def bs2_axpy(alpha: float, x, beta: float, y) -> None:
         L = _lib.lib()
         _lib.check(L.sb_bs2_axpy(float(alpha), x.data_ptr(), float(beta), y.data_ptr(), x.shape[0],
                                  _lib.stream_handle(dev)), "bs2_axpy")
+        return
+    if hoststream.all_host(x, y) and x is not y:
+        hx, hy = hoststream.as_host_tensor(x, "x"), hoststream.as_host_tensor(y, "y")
+        hoststream.run(hx.shape[0], {"x": hx, "y": hy}, {"y": hy}, (),
+                       lambda d, lo, hi: bs2_axpy(alpha, d["x"][lo:hi], beta, d["y"][lo:hi]))
         return
     if x is y:
         sx = _lib.stage(x, torch.float64, "x")
@@ -151,7 +161,9 @@ def bs3_norm2_async(x: DVector, cfg: ReductionConfig = DEFAULT_REDUCTION, out=No
 def bs3_norm2(x, cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
     """kernels.py:106-108: sum(x[i]^2) via the fixed two-stage schedule."""
     if not _all_cuda(x):
-        x = _lib.stage(x, torch.float64, "x").dev
+        hx = hoststream.as_host_tensor(x, "x")
+        return float(hoststream.run(hx.shape[0], {"x": hx}, {}, (),
+                                    final_fn=lambda d: bs3_norm2_async(d["x"], cfg)).item())
     return float(bs3_norm2_async(x, cfg).item())
 
 
@@ -173,6 +185,10 @@ def bs4_dot_async(x: DVector, y: DVector, cfg: ReductionConfig = DEFAULT_REDUCTI
 def bs4_dot(x, y, cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
     """kernels.py:111-114: sum(x[i]*y[i]) via the fixed two-stage schedule."""
     check_same_length(x, y)
+    if hoststream.all_host(x, y):
+        hx, hy = hoststream.as_host_tensor(x, "x"), hoststream.as_host_tensor(y, "y")
+        return float(hoststream.run(hx.shape[0], {"x": hx, "y": hy}, {}, (),
+                                    final_fn=lambda d: bs4_dot_async(d["x"], d["y"], cfg)).item())
     if not _all_cuda(x, y):
         sx, sy = _stage_all(("x", "y"), (x, y))
         x, y = sx.dev, sy.dev
@@ -205,6 +221,19 @@ def bs5_fused_cg_update(alpha: float, p, ap, x, r,
     check_same_length(p, ap, x, r)
     if _all_cuda(p, ap, x, r):
         return float(bs5_fused_cg_update_async(alpha, p, ap, x, r, cfg).item())
+    if hoststream.all_host(p, ap, x, r):
+        # Chunked: per chunk the two rounded updates (bitwise BS5's vectors, SPEC
+        # fusion equivalence); the scalar is the BS3 lattice over the assembled
+        # r_new on the device -- bitwise the fused kernel's (test_kernels.py:194-199).
+        h = {k: hoststream.as_host_tensor(v, k) for k, v in (("p", p), ("ap", ap), ("x", x), ("r", r))}
+
+        def chunk(d, lo, hi):
+            bs2_axpy(alpha, d["p"][lo:hi], 1.0, d["x"][lo:hi])
+            bs2_axpy(-alpha, d["ap"][lo:hi], 1.0, d["r"][lo:hi])
+
+        res = hoststream.run(h["x"].shape[0], h, {"x": h["x"], "r": h["r"]}, (), chunk,
+                             final_fn=lambda d: bs3_norm2_async(d["r"], cfg))
+        return float(res.item())
     staged = _stage_all(("p", "ap", "x", "r"), (p, ap, x, r))
     res = bs5_fused_cg_update_async(alpha, *(s.dev for s in staged), cfg)
     staged[2].writeback()

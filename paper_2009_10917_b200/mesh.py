@@ -229,6 +229,47 @@ def build_gather(mesh: MeshConnectivity, nodes_per_block: int = 512) -> GatherOp
                     nodes_per_block=nodes_per_block)
 
 
+def build_slab_gather(K: int, p: int, z0: int, z1: int, c_lo: int, c_hi: int,
+                      nodes_per_block: int = 512, device=None) -> GatherOp:
+    """Gather operator of a z-slab (multi-GPU partition, dist.py).
+
+    Rows are the global lattice rows of planes [c_lo, c_hi) (renumbered from
+    0), columns the local DOFs of elements with ez in [z0, z1) (renumbered from
+    the slab's first element), entries in the reference's ascending order.  With
+    z0=0, z1=K, c_lo=0, c_hi=K*p+1 this is build_gather(build_mesh(K, p)).
+    """
+    g = K * p + 1
+    dev = _dev(device)
+    ng = (c_hi - c_lo) * g * g
+    nl = K * K * (z1 - z0) * (p + 1) ** 3
+    longest = (2 if K >= 2 else 1) ** 2 * (2 if z1 - z0 >= 2 else 1)
+    if longest > nodes_per_block:
+        raise ValueError(f"nodes_per_block={nodes_per_block} is below the longest row "
+                         f"({longest} nonzeros)")
+    L = _lib.lib()
+    st = _lib.stream_handle(dev)
+    rs = torch.empty(ng + 1, dtype=INDEX_DTYPE, device=dev)
+    ci = torch.empty(nl, dtype=INDEX_DTYPE, device=dev)
+    _lib.check(L.sb_build_gather_csr(K, p, z0, z1, c_lo, c_hi, rs.data_ptr(), ci.data_ptr(), st),
+               "build_slab_gather")
+    nnz = int(rs[-1].item())
+    ci = ci[:nnz]  # entries of planes outside [c_lo, c_hi) are not part of this operator
+    bst = _block_starts(rs, ng, nodes_per_block)
+    return GatherOp(ng=ng, row_starts=rs, col_ids=ci, block_starts=bst,
+                    nodes_per_block=nodes_per_block)
+
+
+def build_slab_l2g(K: int, p: int, z0: int, z1: int, device=None) -> torch.Tensor:
+    """local_to_global (global lattice ids) of the elements with ez in [z0, z1)."""
+    dev = _dev(device)
+    nl = K * K * (z1 - z0) * (p + 1) ** 3
+    l2g = torch.empty(nl, dtype=INDEX_DTYPE, device=dev)
+    L = _lib.lib()
+    _lib.check(L.sb_build_l2g(K, p, z0, z1, l2g.data_ptr(), _lib.stream_handle(dev)),
+               "build_slab_l2g")
+    return l2g
+
+
 def multiplicity(mesh: MeshConnectivity) -> torch.Tensor:
     """mesh.py:150-153: per-global-node count of element-local copies (float64, device)."""
     l2g = mesh.local_to_global
