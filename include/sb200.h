@@ -103,10 +103,10 @@ int sb_bs6_gather(const int32_t *block_starts, int64_t n_blocks, const int32_t *
                   sb_stream_t stream);
 
 /* Pipelined BS6 (the fast path): a per-operator "plan" of super-blocks
- * (G = max(1, 2048 / nodes_per_block) consecutive row blocks each) lets a
+ * (G = max(1, 512 / nodes_per_block) consecutive row blocks each) lets a
  * persistent kernel keep index tiles, value gathers and row sums of three
  * super-blocks in flight.  sb_bs6_plan_size returns the number of int32
- * plan entries (0 if nodes_per_block > 2048: use sb_bs6_gather);
+ * plan entries (0 if nodes_per_block > 512: use sb_bs6_gather);
  * sb_bs6_make_plan fills it once per operator.  row_starts and col_ids must
  * be 16-byte aligned.  Results are bitwise those of sb_bs6_gather. */
 int64_t sb_bs6_plan_size(int64_t n_blocks, int64_t nodes_per_block);

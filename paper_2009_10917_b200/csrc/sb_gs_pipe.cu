@@ -20,7 +20,11 @@
 namespace sb {
 
 constexpr int kPipeT = 256;
-constexpr int kBs6Cap = 2048;  // entries per BS6 super-block (8 per thread)
+// BS6: many small CTAs beat few large ones (measured on B200, K=66 N=7: CAP
+// 2048 x 256 thr x 3 CTA/SM 4.47 TB/s; CAP 512 x 128 thr x 12 CTA/SM 5.72 TB/s)
+constexpr int kBs6T = 128;
+constexpr int kBs6Cap = 512;   // entries per BS6 super-block (4 per thread)
+constexpr int kBs6MinCtas = 12;
 
 // ---- BS7 ----------------------------------------------------------------
 template <int T, int U, bool MASK>
@@ -87,9 +91,12 @@ int bs7_pipe_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bs7_pipe<T, U, true>, T, 0);
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bs7_pipe<T, U, false>, T, 0);
+    // Oversubscribed grid (~64 waves): on B200 hardware CTA scheduling beat a
+    // persistent one-wave grid by 4-20% across N=1..15 (scripts/expt/run_bs7.py);
+    // the ids prefetch then covers the CTAs that take a second tile.
     const int64_t tiles = std::max<int64_t>(1, (n4 + T * U - 1) / (T * U));
-    const unsigned grid =
-        (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count() * std::max(1, per_sm)));
+    const unsigned grid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(tiles, (int64_t)sm_count() * std::max(1, per_sm) * 64));
     const int4 *ids4 = reinterpret_cast<const int4 *>(ids);
     double2 *ql2 = reinterpret_cast<double2 *>(ql);
     if (has_mask)
@@ -129,7 +136,7 @@ __device__ __forceinline__ SbMeta load_meta(const int32_t *plan, int64_t i, int6
 }
 
 template <int T, int CAP>
-__global__ void __launch_bounds__(T, 3) k_bs6_pipe(const int32_t *__restrict__ plan, int64_t nsb,
+__global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pipe(const int32_t *__restrict__ plan, int64_t nsb,
                                                   const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
                                                   const double *__restrict__ q, double *__restrict__ out,
                                                   const double *__restrict__ carry, int64_t ncarry) {
@@ -244,7 +251,7 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     if (ng == 0) return SB_OK;
     if (ncarry > ng) ncarry = ng;
     const int64_t nsb = psize / 2 - 1;
-    constexpr int T = kPipeT;
+    constexpr int T = kBs6T;
     const size_t smem = 2 * kBs6Cap * sizeof(double) + 2 * (kBs6Cap + 4) * sizeof(int32_t);
     static thread_local int attr_dev = -1;
     int dev = 0;

@@ -1,0 +1,88 @@
+// Experimental BS7 variants for A/B timing on the box (not part of libsb200).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+__device__ __forceinline__ uint64_t pol_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+template <int T, int U, int MINB, bool KEEP>
+__global__ void __launch_bounds__(T, MINB) k7(const int4 *__restrict__ ids4, int64_t n4, const double *__restrict__ qg,
+                                              double2 *__restrict__ ql2) {
+    const uint64_t pol = pol_last();
+    const int64_t stride = (int64_t)gridDim.x * T * U;
+    int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x;
+    int4 nxt[U];
+#pragma unroll
+    for (int j = 0; j < U; j++)
+        if (base + j * T < n4) nxt[j] = __ldcs(ids4 + base + j * T);
+    for (; base < n4; base += stride) {
+        int4 cur[U];
+        double v[U][4];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            cur[j] = nxt[j];
+            if (base + j * T < n4) {
+                if (KEEP) {
+                    v[j][0] = ld_keep(qg + cur[j].x, pol);
+                    v[j][1] = ld_keep(qg + cur[j].y, pol);
+                    v[j][2] = ld_keep(qg + cur[j].z, pol);
+                    v[j][3] = ld_keep(qg + cur[j].w, pol);
+                } else {
+                    v[j][0] = __ldg(qg + cur[j].x);
+                    v[j][1] = __ldg(qg + cur[j].y);
+                    v[j][2] = __ldg(qg + cur[j].z);
+                    v[j][3] = __ldg(qg + cur[j].w);
+                }
+            }
+        }
+        const int64_t nb = base + stride;
+#pragma unroll
+        for (int j = 0; j < U; j++)
+            if (nb + j * T < n4) nxt[j] = __ldcs(ids4 + nb + j * T);
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const int64_t i = base + j * T;
+            if (i < n4) {
+                __stcs(ql2 + 2 * i, make_double2(v[j][0], v[j][1]));
+                __stcs(ql2 + 2 * i + 1, make_double2(v[j][2], v[j][3]));
+            }
+        }
+    }
+}
+
+template <int T, int U, int MINB, bool KEEP>
+static int run(const int4 *ids4, int64_t n4, const double *qg, double2 *ql2, int mult, cudaStream_t st) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k7<T, U, MINB, KEEP>, T, 0);
+    int64_t grid = 148LL * per_sm * (mult > 0 ? mult : 1);
+    const int64_t tiles = (n4 + T * U - 1) / (T * U);
+    if (grid > tiles) grid = tiles;
+    k7<T, U, MINB, KEEP><<<(unsigned)grid, T, 0, st>>>(ids4, n4, qg, ql2);
+    return per_sm;
+}
+
+extern "C" int expt_bs7(int variant, const int32_t *ids, int64_t nl, const double *qg, double *ql, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int4 *i4 = reinterpret_cast<const int4 *>(ids);
+    double2 *q2 = reinterpret_cast<double2 *>(ql);
+    const int64_t n4 = nl / 4;
+    switch (variant) {
+        case 0: return run<256, 2, 1, true>(i4, n4, qg, q2, 1, st);
+        case 1: return run<128, 2, 16, true>(i4, n4, qg, q2, 1, st);
+        case 2: return run<256, 4, 1, true>(i4, n4, qg, q2, 1, st);
+        case 3: return run<128, 4, 8, true>(i4, n4, qg, q2, 1, st);
+        case 4: return run<256, 2, 1, false>(i4, n4, qg, q2, 1, st);
+        case 5: return run<256, 1, 8, true>(i4, n4, qg, q2, 1, st);
+        case 6: return run<256, 2, 1, true>(i4, n4, qg, q2, 64, st);  // non-persistent-ish
+        case 7: return run<512, 2, 4, true>(i4, n4, qg, q2, 1, st);
+        default: return -1;
+    }
+}

@@ -201,7 +201,7 @@ def test_pipelined_bs6_matches_unplanned(sb, K, p, npb):
     from paper_2009_10917_b200.gs import bs6_gather_into
     mesh = sb.build_mesh(K, p)
     op = sb.build_gather(mesh, npb)
-    assert op.plan() is not None
+    assert (op.plan() is not None) == (npb <= 512)
     plain = types.SimpleNamespace(ng=op.ng, nl=op.nl, row_starts=op.row_starts, col_ids=op.col_ids,
                                   block_starts=op.block_starts, nodes_per_block=npb,
                                   n_blocks=op.n_blocks)
