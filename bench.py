@@ -332,6 +332,7 @@ def time_steps(w, steps, warmup, barrier, clk=None, settle_s=0.6):
     torch.cuda.synchronize(w.dev)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(TESTS) + 1)] for _ in range(steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects these launches
     start.record(stream)
     for s in range(steps):
         ev[s][0].record(stream)
@@ -339,6 +340,7 @@ def time_steps(w, steps, warmup, barrier, clk=None, settle_s=0.6):
             w.call(t)
             ev[s][i + 1].record(stream)
     stop.record(stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize(w.dev)
     barrier()
     total_ms = start.elapsed_time(stop)
