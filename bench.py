@@ -17,8 +17,13 @@ a K_g x K_g x K_g mesh; BS3-BS5 finish with an NCCL all-gather of the rank
 scalars + a fixed rank-order sum, BS6 with a one-plane carry halo
 (dist.py).
 
---impl reference times the reference algorithm's CPU restatement (the C
-oracle port, all host threads) on a bounded sample of the same workload.
+--impl reference times the reference's CPU implementation restated in numpy
+(oracle/np_port.py: numpy temporaries over a thread pool of all host cores,
+as pkg/src/streambench does) on a bounded sample of the same workload; the
+default arm's cpu_baseline also reports the C/OpenMP restatement (c_port).
+
+SB200_DIST_BACKEND=gloo runs the multi-rank path with several ranks on one
+GPU (host-staged exchanges) -- a functional check; the product uses NCCL.
 """
 
 from __future__ import annotations
@@ -46,8 +51,10 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=float, default=1e8, help="BS1-BS5 DOFs per GPU")
-    ap.add_argument("--K", type=int, default=66, help="BS6/BS7 mesh elements per axis (1 GPU)")
+    # (no option may be a prefix of a torchrun flag: torchrun re-parses abbreviations)
+    ap.add_argument("--dofs", dest="n", type=float, default=1e8, help="BS1-BS5 DOFs per GPU")
+    ap.add_argument("--mesh-k", dest="K", type=int, default=66,
+                    help="BS6/BS7 mesh elements per axis (1 GPU)")
     ap.add_argument("--order", type=int, default=7)
     ap.add_argument("--block-size", type=int, default=256)
     ap.add_argument("--n-blocks", type=int, default=512)
@@ -427,22 +434,31 @@ def main_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    device = torch.device("cuda", local)
+    # SB200_DIST_BACKEND=gloo lets several ranks share one GPU (NCCL refuses
+    # duplicate devices) to exercise the multi-rank path; the product uses NCCL.
+    backend = os.environ.get("SB200_DIST_BACKEND", "nccl")
+    device = torch.device("cuda", local % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(device)
     dist_ctx = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
         from paper_2009_10917_b200 import dist as D
         dist_ctx = D.BenchContext(rank, world, args, device)
 
         def barrier():
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[device.index])
+            else:
+                dist.barrier()
     else:
         def barrier():
             pass
 
     w = Workload(args, device, dist_ctx)
-    with ClockSampler(local) as clk:
+    with ClockSampler(device.index) as clk:
         total_ms, per_ms = time_steps(w, args.steps, args.warmup, barrier, clk)
         time.sleep(0.25)  # let the sampler flush the last interval
     step_ms = total_ms / args.steps
@@ -466,7 +482,10 @@ def main_ours(args):
             "achieved": round(dom_gbs, 1), "peak": peak, "unit": "GB/s",
             "frac": round(dom_gbs / peak, 4), "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
             if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
-            "traffic": traffic_from_profiles(KERNEL_KEYS[dom]),
+            # ncu DRAM bytes per launch, only valid for the profiled configuration
+            "traffic": traffic_from_profiles(KERNEL_KEYS[dom])
+            if (world == 1 and int(args.n) == 100_000_000 and args.K == 66 and args.order == 7
+                and (args.block_size, args.n_blocks) == (256, 512)) else None,
             "algorithmic_bytes_per_launch": w.bytes[dom],
             "min_frac_all_tests": round(min(v["frac_of_peak"] for v in per_test.values()), 4)}
     result = None

@@ -120,11 +120,12 @@ class DistReducer:
         self.sum_fn = sum_fn or _gpu_sum_ordered
 
     def combine(self, local: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        if self.buf.is_cuda:
+        if _nccl(self.group):
             dist.all_gather_into_tensor(self.buf, local.reshape(1), group=self.group)
-        else:  # gloo has no all_gather_into_tensor
-            parts = list(self.buf.split(1))
-            dist.all_gather(parts, local.reshape(1).clone(), group=self.group)
+        else:  # gloo: no all_gather_into_tensor, host tensors only
+            parts = [torch.empty(1, dtype=torch.float64) for _ in range(self.world)]
+            dist.all_gather(parts, local.reshape(1).cpu(), group=self.group)
+            self.buf.copy_(torch.cat(parts))
         res = out if out is not None else torch.empty(1, dtype=torch.float64, device=self.device)
         self.sum_fn(self.buf, res)
         return res
@@ -134,6 +135,34 @@ def _gpu_sum_ordered(values: torch.Tensor, res: torch.Tensor) -> None:
     L = _lib.lib()
     _lib.check(L.sb_sum_ordered(values.data_ptr(), values.shape[0], res.data_ptr(),
                                 _lib.stream_handle(values.device)), "sum_ordered")
+
+
+def _nccl(group) -> bool:
+    return dist.get_backend(group) == "nccl"
+
+
+def _p2p(ops, group) -> None:
+    """Grouped send/recv.  NCCL moves device buffers directly (NVLink); gloo
+    (CPU-only tests, or SB200_DIST_BACKEND=gloo runs of bench.py) stages device
+    buffers through host copies."""
+    if not ops:
+        return
+    if _nccl(group):
+        reqs = dist.batch_isend_irecv([dist.P2POp(fn, t, peer, group=group) for fn, t, peer in ops])
+        for r in reqs:
+            r.wait()
+        return
+    staged = []
+    for fn, t, peer in ops:
+        h = t.cpu() if (fn is dist.isend and t.is_cuda) else (
+            torch.empty(t.shape, dtype=t.dtype) if t.is_cuda else t)
+        staged.append((fn, t, h, peer))
+    reqs = [fn(h, peer, group=group) for fn, _, h, peer in staged]
+    for r in reqs:
+        r.wait()
+    for fn, t, h, _ in staged:
+        if fn is dist.irecv and h is not t:
+            t.copy_(h)
 
 
 def combine_host(values) -> float:
@@ -182,12 +211,10 @@ class DistGather:
     def exchange(self) -> None:
         ops = []
         if self.send_buf is not None:
-            ops.append(dist.P2POp(dist.isend, self.send_buf, self.rank + 1, group=self.group))
+            ops.append((dist.isend, self.send_buf, self.rank + 1))
         if self.carry is not None:
-            ops.append(dist.P2POp(dist.irecv, self.carry, self.rank - 1, group=self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+            ops.append((dist.irecv, self.carry, self.rank - 1))
+        _p2p(ops, self.group)
 
     def gather(self, q_slab: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
         """out (= this rank's rows of the global gathered vector) from q_slab."""
@@ -223,13 +250,10 @@ class DistScatter:
         plane = self.part.plane
         ops = []
         if self.rank > 0:
-            ops.append(dist.P2POp(dist.isend, self.window[:plane], self.rank - 1, group=self.group))
+            ops.append((dist.isend, self.window[:plane], self.rank - 1))
         if self.rank < self.part.world - 1:
-            ops.append(dist.P2POp(dist.irecv, self.window[self.own_rows:], self.rank + 1,
-                                  group=self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+            ops.append((dist.irecv, self.window[self.own_rows:], self.rank + 1))
+        _p2p(ops, self.group)
 
     def scatter(self, q_local: torch.Tensor) -> None:
         """window[:own_rows] must hold this rank's q_global rows."""
