@@ -356,6 +356,26 @@ def time_steps(w, steps, warmup, barrier, clk=None, settle_s=0.6):
     return total_ms, per_ms
 
 
+def time_isolated(w, reps):
+    """Each test alone, `reps` back-to-back calls between CUDA events: the
+    per-kernel figure free of the neighbouring tests' L2 write-backs (in the
+    step, BS3 pays for BS2's dirty lines and BS2 looks faster than it is)."""
+    torch = w.torch
+    stream = torch.cuda.current_stream(w.dev)
+    out = {}
+    for t in TESTS:
+        w.call(t)
+        torch.cuda.synchronize(w.dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            w.call(t)
+        e1.record(stream)
+        e1.synchronize()
+        out[t] = e0.elapsed_time(e1) / reps
+    return out
+
+
 def run_e2e(args, device, steps):
     """Same step through the public API with pinned HOST buffers: every step
     copies its inputs H2D and its outputs (and scalars) D2H inside the timer."""
@@ -461,12 +481,20 @@ def main_ours(args):
     with ClockSampler(device.index) as clk:
         total_ms, per_ms = time_steps(w, args.steps, args.warmup, barrier, clk)
         time.sleep(0.25)  # let the sampler flush the last interval
+    iso_ms = time_isolated(w, max(3, args.steps))
     step_ms = total_ms / args.steps
     if world > 1:
-        t = torch.tensor([step_ms] + [per_ms[k] for k in TESTS], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([step_ms] + [per_ms[k] for k in TESTS] + [iso_ms[k] for k in TESTS],
+                         dtype=torch.float64, device=device)
+        if backend == "nccl":
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        else:
+            tc = t.cpu()
+            dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+            t = tc
         step_ms = float(t[0])
         per_ms = {k: float(t[i + 1]) for i, k in enumerate(TESTS)}
+        iso_ms = {k: float(t[len(TESTS) + i + 1]) for i, k in enumerate(TESTS)}
     bytes_step = sum(w.bytes.values()) * world
     value = bytes_step / (step_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
@@ -474,8 +502,10 @@ def main_ours(args):
     per_test = {}
     for k in TESTS:
         gbs = w.bytes[k] * world / (per_ms[k] * 1e-3) / 1e9
+        iso = w.bytes[k] * world / (iso_ms[k] * 1e-3) / 1e9
         per_test[k] = {"GBps": round(gbs, 1), "frac_of_peak": round(gbs / agg_peak, 4),
-                       "ms": round(per_ms[k], 4), "bytes_per_rank": w.bytes[k]}
+                       "ms": round(per_ms[k], 4), "bytes_per_rank": w.bytes[k],
+                       "GBps_isolated": round(iso, 1), "frac_isolated": round(iso / agg_peak, 4)}
     dom = max(TESTS, key=lambda k: per_ms[k])
     dom_gbs = w.bytes[dom] / (per_ms[dom] * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": KERNEL_KEYS[dom], "test": dom,

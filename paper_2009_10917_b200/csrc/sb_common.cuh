@@ -26,7 +26,7 @@ inline int launch_check(const char *what) { return cuda_check(cudaGetLastError()
 
 inline cudaStream_t as_stream(sb_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
-inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+__host__ __device__ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 constexpr int kSMs = 148;  // B200; grids are sized from the device query at runtime
 
@@ -55,6 +55,11 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 __device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
     double v;
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double2 ld2_keep(const double *p, uint64_t pol) {
+    double2 v;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
     return v;
 }
 

@@ -27,6 +27,39 @@ constexpr int kBs6Cap = 512;   // entries per BS6 super-block (4 per thread)
 constexpr int kBs6MinCtas = 12;
 
 // ---- BS7 ----------------------------------------------------------------
+// Gather of a thread's 4 consecutive local entries.  Element-local numbering
+// makes them consecutive global ids along an element edge (an i-run), so when
+// they are, the values come in 16 B loads (half the load instructions; the
+// sectors fetched are the same).
+__device__ __forceinline__ void gather4(const double *qg, int4 d, uint64_t pol, double *v) {
+    if (d.y == d.x + 1 && d.z == d.x + 2 && d.w == d.x + 3) {
+        if (aligned16(qg + d.x)) {
+            const double2 a = ld2_keep(qg + d.x, pol), b = ld2_keep(qg + d.x + 2, pol);
+            v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+        } else {
+            v[0] = ld_keep(qg + d.x, pol);
+            const double2 m = ld2_keep(qg + d.x + 1, pol);
+            v[1] = m.x; v[2] = m.y;
+            v[3] = ld_keep(qg + d.w, pol);
+        }
+        return;
+    }
+    if (d.y == d.x + 1 && aligned16(qg + d.x)) {
+        const double2 a = ld2_keep(qg + d.x, pol);
+        v[0] = a.x; v[1] = a.y;
+    } else {
+        v[0] = ld_keep(qg + d.x, pol);
+        v[1] = ld_keep(qg + d.y, pol);
+    }
+    if (d.w == d.z + 1 && aligned16(qg + d.z)) {
+        const double2 b = ld2_keep(qg + d.z, pol);
+        v[2] = b.x; v[3] = b.y;
+    } else {
+        v[2] = ld_keep(qg + d.z, pol);
+        v[3] = ld_keep(qg + d.w, pol);
+    }
+}
+
 template <int T, int U, bool MASK>
 __global__ void __launch_bounds__(T) k_bs7_pipe(const int4 *__restrict__ ids4, int64_t n4,
                                                const double *__restrict__ qg, double2 *__restrict__ ql2,
@@ -46,10 +79,14 @@ __global__ void __launch_bounds__(T) k_bs7_pipe(const int4 *__restrict__ ids4, i
         for (int j = 0; j < U; j++) {
             cur[j] = nxt[j];
             if (base + j * T < n4) {
-                if (!MASK || cur[j].x >= 0) v[j][0] = ld_keep(qg + cur[j].x, pol);
-                if (!MASK || cur[j].y >= 0) v[j][1] = ld_keep(qg + cur[j].y, pol);
-                if (!MASK || cur[j].z >= 0) v[j][2] = ld_keep(qg + cur[j].z, pol);
-                if (!MASK || cur[j].w >= 0) v[j][3] = ld_keep(qg + cur[j].w, pol);
+                if (!MASK) {
+                    gather4(qg, cur[j], pol, v[j]);
+                } else {
+                    if (cur[j].x >= 0) v[j][0] = ld_keep(qg + cur[j].x, pol);
+                    if (cur[j].y >= 0) v[j][1] = ld_keep(qg + cur[j].y, pol);
+                    if (cur[j].z >= 0) v[j][2] = ld_keep(qg + cur[j].z, pol);
+                    if (cur[j].w >= 0) v[j][3] = ld_keep(qg + cur[j].w, pol);
+                }
             }
         }
         const int64_t nb = base + stride;  // prefetch the next tile's ids
@@ -84,7 +121,9 @@ __global__ void __launch_bounds__(T) k_bs7_pipe(const int4 *__restrict__ ids4, i
 
 int bs7_pipe_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,
                     cudaStream_t st) {
-    constexpr int T = kPipeT, U = 2;
+    // 128-thread CTAs, 2 x int4 of ids each, contiguity-aware gathers: best of
+    // the variants measured in scripts/expt/run_bs7.py (N = 1, 3, 7, 15)
+    constexpr int T = 128, U = 2;
     const int64_t n4 = nl / 4;
     int per_sm = 1;
     if (has_mask)
@@ -137,10 +176,12 @@ __device__ __forceinline__ SbMeta load_meta(const int32_t *plan, int64_t i, int6
 
 template <int T, int CAP>
 __global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pipe(const int32_t *__restrict__ plan, int64_t nsb,
-                                                  const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
-                                                  const double *__restrict__ q, double *__restrict__ out,
-                                                  const double *__restrict__ carry, int64_t ncarry) {
-    constexpr int M = CAP / T;             // entries per thread
+                                                            const int32_t *__restrict__ rs,
+                                                            const int32_t *__restrict__ ci,
+                                                            const double *__restrict__ q,
+                                                            double *__restrict__ out,
+                                                            const double *__restrict__ carry, int64_t ncarry) {
+    constexpr int M = CAP / (2 * T);          // entry pairs per thread
     constexpr int R = (CAP + 1 + T - 1) / T;  // row starts per thread (rows <= CAP)
     extern __shared__ __align__(16) unsigned char bs6_smem[];
     double(*qs)[CAP] = reinterpret_cast<double(*)[CAP]>(bs6_smem);
@@ -150,22 +191,34 @@ __global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pipe(const int32_t *__re
     int64_t sbi = blockIdx.x;
     SbMeta mc = load_meta(plan, sbi, nsb);      // current super-block
     SbMeta mn = load_meta(plan, sbi + g, nsb);  // next
-    int32_t cols[M];
+    int2 cols[M];  // each thread owns consecutive entries (2k, 2k+1)
 #pragma unroll
     for (int m = 0; m < M; m++) {
-        const int k = threadIdx.x + m * T;
-        if (k < mc.e1 - mc.e0) cols[m] = ld_stream(ci + mc.e0 + k);
+        const int k = 2 * (threadIdx.x + m * T), ne = mc.e1 - mc.e0;
+        if (k < ne) cols[m].x = ld_stream(ci + mc.e0 + k);
+        if (k + 1 < ne) cols[m].y = ld_stream(ci + mc.e0 + k + 1);
     }
     int buf = 0;
     for (; sbi < nsb; sbi += g) {
         const int ne = mc.e1 - mc.e0, nrows = mc.r1 - mc.r0;
-        // A: value gathers of this super-block; B: its row starts
-        double v[M];
+        // A: value gathers of this super-block -- one 16 B load when the pair's
+        //    columns are consecutive (an element edge), else two 8 B loads
+        double2 v[M];
 #pragma unroll
         for (int m = 0; m < M; m++) {
-            const int k = threadIdx.x + m * T;
-            if (k < ne) v[m] = __ldg(q + cols[m]);
+            const int k = 2 * (threadIdx.x + m * T);
+            if (k + 1 < ne) {
+                if (cols[m].y == cols[m].x + 1 && aligned16(q + cols[m].x)) {
+                    v[m] = __ldg(reinterpret_cast<const double2 *>(q + cols[m].x));
+                } else {
+                    v[m].x = __ldg(q + cols[m].x);
+                    v[m].y = __ldg(q + cols[m].y);
+                }
+            } else if (k < ne) {
+                v[m].x = __ldg(q + cols[m].x);
+            }
         }
+        // B: row starts of this super-block
         int32_t rv[R];
 #pragma unroll
         for (int j = 0; j < R; j++) {
@@ -176,15 +229,19 @@ __global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pipe(const int32_t *__re
         const int nne = mn.e1 - mn.e0;
 #pragma unroll
         for (int m = 0; m < M; m++) {
-            const int k = threadIdx.x + m * T;
-            if (k < nne) cols[m] = ld_stream(ci + mn.e0 + k);
+            const int k = 2 * (threadIdx.x + m * T);
+            if (k < nne) cols[m].x = ld_stream(ci + mn.e0 + k);
+            if (k + 1 < nne) cols[m].y = ld_stream(ci + mn.e0 + k + 1);
         }
         const SbMeta mnn = load_meta(plan, sbi + 2 * g, nsb);
         // E: publish A/B to shared memory
 #pragma unroll
         for (int m = 0; m < M; m++) {
-            const int k = threadIdx.x + m * T;
-            if (k < ne) qs[buf][k] = v[m];
+            const int k = 2 * (threadIdx.x + m * T);
+            if (k + 1 < ne)
+                *reinterpret_cast<double2 *>(&qs[buf][k]) = v[m];
+            else if (k < ne)
+                qs[buf][k] = v[m].x;
         }
 #pragma unroll
         for (int j = 0; j < R; j++) {

@@ -98,6 +98,96 @@ __global__ void __launch_bounds__(T, MINB) k_pipe(const int32_t *__restrict__ pl
     }
 }
 
+// pairs of consecutive entries per thread; 16 B gathers when the two columns are consecutive
+template <int T, int CAP, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_pipe2(const int32_t *__restrict__ plan, int64_t nsb,
+                                                   const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
+                                                   const double *__restrict__ q, double *__restrict__ out) {
+    constexpr int M = CAP / (2 * T);  // pairs per thread
+    constexpr int R = (CAP + 1 + T - 1) / T;
+    extern __shared__ __align__(16) unsigned char smem[];
+    double(*qs)[CAP] = reinterpret_cast<double(*)[CAP]>(smem);
+    int32_t(*rss)[CAP + 4] = reinterpret_cast<int32_t(*)[CAP + 4]>(smem + 2 * CAP * sizeof(double));
+    const int64_t g = gridDim.x;
+    int64_t sbi = blockIdx.x;
+    SbMeta mc = load_meta(plan, sbi, nsb), mn = load_meta(plan, sbi + g, nsb);
+    int2 cols[M];
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        const int k = 2 * (threadIdx.x + m * T);
+        const int ne = mc.e1 - mc.e0;
+        if (k < ne) cols[m].x = __ldcs(ci + mc.e0 + k);
+        if (k + 1 < ne) cols[m].y = __ldcs(ci + mc.e0 + k + 1);
+    }
+    int buf = 0;
+    for (; sbi < nsb; sbi += g) {
+        const int ne = mc.e1 - mc.e0, nrows = mc.r1 - mc.r0;
+        double2 v[M];
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int k = 2 * (threadIdx.x + m * T);
+            if (k + 1 < ne) {
+                if (cols[m].y == cols[m].x + 1 && (cols[m].x & 1) == 0) {
+                    v[m] = __ldg(reinterpret_cast<const double2 *>(q + cols[m].x));
+                } else {
+                    v[m].x = __ldg(q + cols[m].x);
+                    v[m].y = __ldg(q + cols[m].y);
+                }
+            } else if (k < ne) {
+                v[m].x = __ldg(q + cols[m].x);
+            }
+        }
+        int32_t rv[R];
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+            const int k = threadIdx.x + j * T;
+            if (k <= nrows) rv[j] = __ldcs(rs + mc.r0 + k);
+        }
+        const int nne = mn.e1 - mn.e0;
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int k = 2 * (threadIdx.x + m * T);
+            if (k < nne) cols[m].x = __ldcs(ci + mn.e0 + k);
+            if (k + 1 < nne) cols[m].y = __ldcs(ci + mn.e0 + k + 1);
+        }
+        const SbMeta mnn = load_meta(plan, sbi + 2 * g, nsb);
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const int k = 2 * (threadIdx.x + m * T);
+            if (k + 1 < ne) *reinterpret_cast<double2 *>(&qs[buf][k]) = v[m];
+            else if (k < ne) qs[buf][k] = v[m].x;
+        }
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+            const int k = threadIdx.x + j * T;
+            if (k <= nrows) rss[buf][k] = rv[j];
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < nrows; k += T) {
+            double acc = 0.0;
+            const int a = rss[buf][k] - mc.e0, b = rss[buf][k + 1] - mc.e0;
+            for (int c = a; c < b; c++) acc = add(acc, qs[buf][c]);
+            __stcs(out + mc.r0 + k, acc);
+        }
+        buf ^= 1;
+        mc = mn;
+        mn = mnn;
+    }
+}
+
+template <int CAP, int MINB, int T>
+static int run2(const int32_t *plan, int64_t nsb, const int32_t *rs, const int32_t *ci, const double *q, double *out,
+                cudaStream_t st) {
+    const size_t smem = 2 * CAP * sizeof(double) + 2 * (CAP + 4) * sizeof(int32_t);
+    cudaFuncSetAttribute(k_pipe2<T, CAP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pipe2<T, CAP, MINB>, T, smem);
+    int64_t grid = 148LL * per_sm;
+    if (grid > nsb) grid = nsb;
+    k_pipe2<T, CAP, MINB><<<(unsigned)grid, T, smem, st>>>(plan, nsb, rs, ci, q, out);
+    return per_sm;
+}
+
 template <int CAP, bool SUMS, bool CONTIG, int MINB, int T = 256>
 static int run(const int32_t *plan, int64_t nsb, const int32_t *rs, const int32_t *ci, const double *q, double *out,
                int ctas_per_sm, cudaStream_t st) {
@@ -130,6 +220,9 @@ extern "C" int expt_bs6(int variant, const int32_t *plan, int64_t nsb, const int
         case 9: return run<1024, true, false, 4, 512>(plan, nsb, rs, ci, q, out, ctas_per_sm, st);
         case 10: return run<1024, true, false, 6, 256>(plan, nsb, rs, ci, q, out, ctas_per_sm, st);
         case 11: return run<512, false, false, 8>(plan, nsb, rs, ci, q, out, ctas_per_sm, st);
+        case 12: return run2<512, 12, 128>(plan, nsb, rs, ci, q, out, st);
+        case 13: return run2<512, 16, 128>(plan, nsb, rs, ci, q, out, st);
+        case 14: return run2<1024, 8, 256>(plan, nsb, rs, ci, q, out, st);
         default: return -1;
     }
 }

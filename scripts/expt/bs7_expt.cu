@@ -13,7 +13,35 @@ __device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
     return v;
 }
 
-template <int T, int U, int MINB, bool KEEP>
+__device__ __forceinline__ double2 ld2_keep(const double *p, uint64_t pol) {
+    double2 v;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
+// contiguity-aware gather of 4 ids: 16 B loads where ids run consecutively
+__device__ __forceinline__ void gather4(const double *qg, int4 d, uint64_t pol, double *v) {
+    if (d.y == d.x + 1 && d.z == d.x + 2 && d.w == d.x + 3) {
+        if ((d.x & 1) == 0) {
+            const double2 a = ld2_keep(qg + d.x, pol), b = ld2_keep(qg + d.x + 2, pol);
+            v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+        } else {
+            v[0] = ld_keep(qg + d.x, pol);
+            const double2 m = ld2_keep(qg + d.x + 1, pol);
+            v[1] = m.x; v[2] = m.y;
+            v[3] = ld_keep(qg + d.w, pol);
+        }
+        return;
+    }
+    if (d.y == d.x + 1 && (d.x & 1) == 0) {
+        const double2 a = ld2_keep(qg + d.x, pol); v[0] = a.x; v[1] = a.y;
+    } else { v[0] = ld_keep(qg + d.x, pol); v[1] = ld_keep(qg + d.y, pol); }
+    if (d.w == d.z + 1 && (d.z & 1) == 0) {
+        const double2 b = ld2_keep(qg + d.z, pol); v[2] = b.x; v[3] = b.y;
+    } else { v[2] = ld_keep(qg + d.z, pol); v[3] = ld_keep(qg + d.w, pol); }
+}
+
+template <int T, int U, int MINB, bool KEEP, bool VEC = false>
 __global__ void __launch_bounds__(T, MINB) k7(const int4 *__restrict__ ids4, int64_t n4, const double *__restrict__ qg,
                                               double2 *__restrict__ ql2) {
     const uint64_t pol = pol_last();
@@ -30,7 +58,9 @@ __global__ void __launch_bounds__(T, MINB) k7(const int4 *__restrict__ ids4, int
         for (int j = 0; j < U; j++) {
             cur[j] = nxt[j];
             if (base + j * T < n4) {
-                if (KEEP) {
+                if (VEC) {
+                    gather4(qg, cur[j], pol, v[j]);
+                } else if (KEEP) {
                     v[j][0] = ld_keep(qg + cur[j].x, pol);
                     v[j][1] = ld_keep(qg + cur[j].y, pol);
                     v[j][2] = ld_keep(qg + cur[j].z, pol);
@@ -58,14 +88,14 @@ __global__ void __launch_bounds__(T, MINB) k7(const int4 *__restrict__ ids4, int
     }
 }
 
-template <int T, int U, int MINB, bool KEEP>
+template <int T, int U, int MINB, bool KEEP, bool VEC = false>
 static int run(const int4 *ids4, int64_t n4, const double *qg, double2 *ql2, int mult, cudaStream_t st) {
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k7<T, U, MINB, KEEP>, T, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k7<T, U, MINB, KEEP, VEC>, T, 0);
     int64_t grid = 148LL * per_sm * (mult > 0 ? mult : 1);
     const int64_t tiles = (n4 + T * U - 1) / (T * U);
     if (grid > tiles) grid = tiles;
-    k7<T, U, MINB, KEEP><<<(unsigned)grid, T, 0, st>>>(ids4, n4, qg, ql2);
+    k7<T, U, MINB, KEEP, VEC><<<(unsigned)grid, T, 0, st>>>(ids4, n4, qg, ql2);
     return per_sm;
 }
 
@@ -83,6 +113,9 @@ extern "C" int expt_bs7(int variant, const int32_t *ids, int64_t nl, const doubl
         case 5: return run<256, 1, 8, true>(i4, n4, qg, q2, 1, st);
         case 6: return run<256, 2, 1, true>(i4, n4, qg, q2, 64, st);  // non-persistent-ish
         case 7: return run<512, 2, 4, true>(i4, n4, qg, q2, 1, st);
+        case 8: return run<256, 2, 1, true, true>(i4, n4, qg, q2, 64, st);
+        case 9: return run<256, 4, 1, true, true>(i4, n4, qg, q2, 64, st);
+        case 10: return run<128, 2, 1, true, true>(i4, n4, qg, q2, 64, st);
         default: return -1;
     }
 }

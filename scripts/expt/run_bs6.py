@@ -38,8 +38,7 @@ for K, p in [(66, 7), (463, 1), (31, 15)]:
     nbytes = bytes_moved("bs6", nl=mesh.nl, ng=mesh.ng)
     out = torch.empty_like(ref)
     st = torch.cuda.current_stream()
-    for variant, cap, cps in [(0, 2048, 0), (5, 512, 0), (6, 512, 0), (7, 512, 0), (9, 1024, 0),
-                              (10, 1024, 0), (11, 512, 0)]:
+    for variant, cap, cps in [(7, 512, 0), (12, 512, 0), (13, 512, 0), (14, 1024, 0), (11, 512, 0)]:
         plan, nsb = plan_for(op, max(1, cap // 512))
         per_sm = L.expt_bs6(variant, plan.data_ptr(), nsb, op.row_starts.data_ptr(), op.col_ids.data_ptr(),
                             q.data_ptr(), out.data_ptr(), cps, st.cuda_stream)

@@ -27,7 +27,7 @@ for K, p in [(66, 7), (463, 1), (31, 15), (132, 3)]:
     nbytes = bytes_moved("bs7", nl=mesh.nl, ng=mesh.ng)
     ql = torch.empty(mesh.nl, dtype=torch.float64, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
-    for variant in range(8):
+    for variant in (0, 6, 8, 9, 10):
         per_sm = L.expt_bs7(variant, ids.ids.data_ptr(), mesh.nl, qg.data_ptr(), ql.data_ptr(), st)
         torch.cuda.synchronize()
         ok = torch.equal(ql, ref)
