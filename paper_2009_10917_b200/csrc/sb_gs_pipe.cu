@@ -174,7 +174,18 @@ __device__ __forceinline__ SbMeta load_meta(const int32_t *plan, int64_t i, int6
     return m;
 }
 
-template <int T, int CAP>
+// Shared-memory slot of super-block entry k.  With long rows (p = 1: 8
+// entries) the one-thread-per-row sums read qs[8l + j] across lanes l -- a
+// 16-way bank conflict; XOR-ing the low 4 bits of the double index with bits
+// 4..7 makes those reads 2 wavefronts (the minimum for 32 x 8 B).  Rows of
+// length 1-2 (p >= 3) are already conflict-light, so SWZ is chosen per
+// operator from the mean row length.
+template <bool SWZ>
+__device__ __forceinline__ int qslot(int k) {
+    return SWZ ? (k ^ ((k >> 4) & 15)) : k;
+}
+
+template <int T, int CAP, bool SWZ>
 __global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pipe(const int32_t *__restrict__ plan, int64_t nsb,
                                                             const int32_t *__restrict__ rs,
                                                             const int32_t *__restrict__ ci,
@@ -238,10 +249,14 @@ __global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pipe(const int32_t *__re
 #pragma unroll
         for (int m = 0; m < M; m++) {
             const int k = 2 * (threadIdx.x + m * T);
-            if (k + 1 < ne)
+            if (SWZ) {
+                if (k < ne) qs[buf][qslot<SWZ>(k)] = v[m].x;
+                if (k + 1 < ne) qs[buf][qslot<SWZ>(k + 1)] = v[m].y;
+            } else if (k + 1 < ne) {
                 *reinterpret_cast<double2 *>(&qs[buf][k]) = v[m];
-            else if (k < ne)
+            } else if (k < ne) {
                 qs[buf][k] = v[m].x;
+            }
         }
 #pragma unroll
         for (int j = 0; j < R; j++) {
@@ -254,7 +269,7 @@ __global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pipe(const int32_t *__re
             const int a = rss[buf][k] - mc.e0, b = rss[buf][k + 1] - mc.e0;
             const int64_t r = (int64_t)mc.r0 + k;
             double acc = r < ncarry ? carry[r] : 0.0;
-            for (int c = a; c < b; c++) acc = add(acc, qs[buf][c]);
+            for (int c = a; c < b; c++) acc = add(acc, qs[buf][qslot<SWZ>(c)]);
             st_stream(out + r, acc);
         }
         buf ^= 1;  // the barrier of the next iteration separates reuse of this buffer
@@ -314,17 +329,22 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     int dev = 0;
     cudaGetDevice(&dev);
     if (attr_dev != dev) {
-        if (cuda_check(cudaFuncSetAttribute(k_bs6_pipe<T, kBs6Cap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem),
+        if (cuda_check(cudaFuncSetAttribute(k_bs6_pipe<T, kBs6Cap, false>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                       "sb_bs6_gather_planned: shared memory attribute") ||
+            cuda_check(cudaFuncSetAttribute(k_bs6_pipe<T, kBs6Cap, true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                        "sb_bs6_gather_planned: shared memory attribute"))
             return SB_E_CUDA;
         attr_dev = dev;
     }
+    const bool swz = nl >= 4 * ng;  // mean row length >= 4 (p = 1 meshes)
+    auto kern = swz ? k_bs6_pipe<T, kBs6Cap, true> : k_bs6_pipe<T, kBs6Cap, false>;
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bs6_pipe<T, kBs6Cap>, T, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
     const int64_t grid = std::min<int64_t>(nsb, (int64_t)sm_count() * std::max(1, per_sm));
-    k_bs6_pipe<T, kBs6Cap><<<(unsigned)std::max<int64_t>(1, grid), T, smem, as_stream(s)>>>(
-        plan, nsb, rs, ci, q, out, carry, ncarry);
+    kern<<<(unsigned)std::max<int64_t>(1, grid), T, smem, as_stream(s)>>>(plan, nsb, rs, ci, q, out, carry,
+                                                                          ncarry);
     return launch_check("sb_bs6_gather_planned");
 }
 
