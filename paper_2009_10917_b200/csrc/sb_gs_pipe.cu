@@ -9,17 +9,25 @@
 // the current tile's value gathers are in flight, so every iteration exposes a
 // single round trip and ~30 KB per CTA stay in flight.  (A cp.async/LDGSTS
 // 3-stage variant of this pipeline was measured slower: MIO-throttle bound on
-// the 8-byte gathers.)
+// the 8-byte gathers; so was a two-deep variant that overlapped one
+// super-block's row sums with the next one's gathers.)
+//
+// BS6 is L1-throughput bound, not DRAM bound (ncu at N=7: l1tex 78% busy,
+// DRAM 66%): every gather instruction costs one L1 tag lookup per distinct
+// 128 B line its lanes touch, and the one-thread-per-row sums cost shared
+// memory wavefronts.  The kernels below are shaped to cut both (see
+// scripts/expt/bs6_diag.cu and profiles/r01_bs6_variants.md).
 //
 // Results are bitwise those of the one-tile kernels: BS6 still sums each row
 // in ascending column order from +0.0 (or the carry-in) in one thread.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "sb_common.cuh"
 
 namespace sb {
 
-constexpr int kPipeT = 256;
 // BS6: many small CTAs beat few large ones (measured on B200, K=66 N=7: CAP
 // 2048 x 256 thr x 3 CTA/SM 4.47 TB/s; CAP 512 x 128 thr x 12 CTA/SM 5.72 TB/s)
 constexpr int kBs6T = 128;
@@ -177,102 +185,201 @@ __device__ __forceinline__ SbMeta load_meta(const int32_t *plan, int64_t i, int6
 // Shared-memory slot of super-block entry k.  With long rows (p = 1: 8
 // entries) the one-thread-per-row sums read qs[8l + j] across lanes l -- a
 // 16-way bank conflict; XOR-ing the low 4 bits of the double index with bits
-// 4..7 makes those reads 2 wavefronts (the minimum for 32 x 8 B).  Rows of
-// length 1-2 (p >= 3) are already conflict-light, so SWZ is chosen per
-// operator from the mean row length.
+// 4..7 makes those reads 2 wavefronts (the minimum for 32 x 8 B).  For the
+// 1-2 entry rows of p >= 7 the lanes' first entries spread over ~48-90
+// doubles and collide 3-4 ways; the same swizzle measured +7% there, and
+// -5% at p = 3..5, so SWZ is chosen per operator from the mean row length.
 template <bool SWZ>
 __device__ __forceinline__ int qslot(int k) {
     return SWZ ? (k ^ ((k >> 4) & 15)) : k;
 }
 
 template <int T, int CAP, bool SWZ>
-__global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pipe(const int32_t *__restrict__ plan, int64_t nsb,
-                                                            const int32_t *__restrict__ rs,
-                                                            const int32_t *__restrict__ ci,
-                                                            const double *__restrict__ q,
-                                                            double *__restrict__ out,
-                                                            const double *__restrict__ carry, int64_t ncarry) {
-    constexpr int M = CAP / (2 * T);          // entry pairs per thread
-    constexpr int R = (CAP + 1 + T - 1) / T;  // row starts per thread (rows <= CAP)
+__device__ __forceinline__ void bs6_issue_vals(const SbMeta &m, const int2 (&cols)[CAP / (2 * T)],
+                                               const double *__restrict__ q, double2 (&v)[CAP / (2 * T)]) {
+    constexpr int M = CAP / (2 * T);
+    const int ne = m.e1 - m.e0;
+#pragma unroll
+    for (int j = 0; j < M; j++) {
+        const int k = 2 * (threadIdx.x + j * T);
+        if (k + 1 < ne) {
+            if (cols[j].y == cols[j].x + 1 && aligned16(q + cols[j].x)) {
+                v[j] = __ldg(reinterpret_cast<const double2 *>(q + cols[j].x));
+            } else {
+                v[j].x = __ldg(q + cols[j].x);
+                v[j].y = __ldg(q + cols[j].y);
+            }
+        } else if (k < ne) {
+            v[j].x = __ldg(q + cols[j].x);
+        }
+    }
+}
+
+template <int T, int CAP>
+__device__ __forceinline__ void bs6_issue_cols(const SbMeta &m, const int32_t *__restrict__ ci,
+                                               int2 (&cols)[CAP / (2 * T)]) {
+    constexpr int M = CAP / (2 * T);
+    const int ne = m.e1 - m.e0;
+#pragma unroll
+    for (int j = 0; j < M; j++) {
+        const int k = 2 * (threadIdx.x + j * T);
+        if (k < ne) cols[j].x = ld_stream(ci + m.e0 + k);
+        if (k + 1 < ne) cols[j].y = ld_stream(ci + m.e0 + k + 1);
+    }
+}
+
+// Row starts stay in registers: thread t owns rows t + j*T of its
+// super-block; the end of row k is the start of row k+1 (a shuffle; lane 31
+// loads it).  The row loop is not unrolled (rows are 1-8 entries long) and
+// output / carry addressing is 32-bit per super-block.
+template <int T, int CAP>
+struct Bs6Rows {
+    static constexpr int R = (CAP + T - 1) / T;  // rows per thread (rows <= CAP)
+    int32_t lo[R], hi31[R];                      // row start; lane 31: start of the next row
+};
+
+template <int T, int CAP>
+__device__ __forceinline__ void bs6_load_rows(const SbMeta &m, const int32_t *__restrict__ rs,
+                                              Bs6Rows<T, CAP> &rw) {
+    const int nrows = m.r1 - m.r0;
+    const int32_t *base = rs + m.r0;
+    const bool last = (threadIdx.x & 31) == 31;
+#pragma unroll
+    for (int j = 0; j < Bs6Rows<T, CAP>::R; j++) {
+        const int k = threadIdx.x + j * T;
+        if (k <= nrows) rw.lo[j] = ld_stream(base + k);  // row k+1's start ends row k
+        if (last && k < nrows) rw.hi31[j] = __ldg(base + k + 1);
+    }
+}
+
+template <int T, int CAP, bool SWZ>
+__device__ __forceinline__ void bs6_row_sums(const SbMeta &m, const Bs6Rows<T, CAP> &rw, const double *qs,
+                                             double *__restrict__ out, const double *__restrict__ carry,
+                                             int64_t ncarry) {
+    const int nrows = m.r1 - m.r0;
+    const bool last = (threadIdx.x & 31) == 31;
+    double *ob = out + m.r0;
+    const int ncar = ncarry > m.r0 ? (int)std::min<int64_t>(ncarry - m.r0, (int64_t)nrows) : 0;
+    const double *cb = carry + m.r0;
+#pragma unroll
+    for (int j = 0; j < Bs6Rows<T, CAP>::R; j++) {
+        const int k = threadIdx.x + j * T;
+        int b = __shfl_down_sync(0xffffffffu, rw.lo[j], 1);
+        if (last) b = rw.hi31[j];
+        if (k < nrows) {
+            int c = rw.lo[j] - m.e0;
+            b -= m.e0;
+            double acc = k < ncar ? cb[k] : 0.0;
+#pragma unroll 1
+            for (; c < b; c++) acc = add(acc, qs[qslot<SWZ>(c)]);
+            st_stream(ob + k, acc);
+        }
+    }
+}
+
+template <int T, int CAP, bool SWZ>
+__device__ __forceinline__ void bs6_publish_vals(const SbMeta &m, const double2 (&v)[CAP / (2 * T)], double *qs) {
+    constexpr int M = CAP / (2 * T);
+    const int ne = m.e1 - m.e0;
+#pragma unroll
+    for (int j = 0; j < M; j++) {
+        const int k = 2 * (threadIdx.x + j * T);
+        if (SWZ) {
+            if (k < ne) qs[qslot<SWZ>(k)] = v[j].x;
+            if (k + 1 < ne) qs[qslot<SWZ>(k + 1)] = v[j].y;
+        } else if (k + 1 < ne) {
+            *reinterpret_cast<double2 *>(&qs[k]) = v[j];
+        } else if (k < ne) {
+            qs[k] = v[j].x;
+        }
+    }
+}
+
+// Pairs kernel (long rows, p <= 1): thread t owns the entry pairs (2t, 2t+1)
+// and (2t+2T, 2t+2T+1) of its super-block, gathered with one 16 B load when
+// the two columns are adjacent (the 8-entry rows of p = 1 meshes pair up
+// often enough for that to beat one entry per lane).
+template <int T, int CAP, bool SWZ>
+__global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pairs(const int32_t *__restrict__ plan, int64_t nsb,
+                                                             const int32_t *__restrict__ rs,
+                                                             const int32_t *__restrict__ ci,
+                                                             const double *__restrict__ q,
+                                                             double *__restrict__ out,
+                                                             const double *__restrict__ carry, int64_t ncarry) {
+    constexpr int M = CAP / (2 * T);
     extern __shared__ __align__(16) unsigned char bs6_smem[];
     double(*qs)[CAP] = reinterpret_cast<double(*)[CAP]>(bs6_smem);
-    int32_t(*rss)[CAP + 4] = reinterpret_cast<int32_t(*)[CAP + 4]>(bs6_smem + 2 * CAP * sizeof(double));
-
     const int64_t g = gridDim.x;
     int64_t sbi = blockIdx.x;
-    SbMeta mc = load_meta(plan, sbi, nsb);      // current super-block
-    SbMeta mn = load_meta(plan, sbi + g, nsb);  // next
-    int2 cols[M];  // each thread owns consecutive entries (2k, 2k+1)
-#pragma unroll
-    for (int m = 0; m < M; m++) {
-        const int k = 2 * (threadIdx.x + m * T), ne = mc.e1 - mc.e0;
-        if (k < ne) cols[m].x = ld_stream(ci + mc.e0 + k);
-        if (k + 1 < ne) cols[m].y = ld_stream(ci + mc.e0 + k + 1);
-    }
+    if (sbi >= nsb) return;
+    int2 cols[M];
+    double2 v[M];
+    Bs6Rows<T, CAP> rw;
     int buf = 0;
+    SbMeta mc = load_meta(plan, sbi, nsb), mn = load_meta(plan, sbi + g, nsb);
+    bs6_issue_cols<T, CAP>(mc, ci, cols);
     for (; sbi < nsb; sbi += g) {
-        const int ne = mc.e1 - mc.e0, nrows = mc.r1 - mc.r0;
-        // A: value gathers of this super-block -- one 16 B load when the pair's
-        //    columns are consecutive (an element edge), else two 8 B loads
-        double2 v[M];
+        bs6_issue_vals<T, CAP, SWZ>(mc, cols, q, v);  // A: values of this super-block
+        bs6_load_rows<T, CAP>(mc, rs, rw);             // B: its row starts
+        bs6_issue_cols<T, CAP>(mn, ci, cols);          // C: indices of the next one
+        const SbMeta mnn = load_meta(plan, sbi + 2 * g, nsb);
+        bs6_publish_vals<T, CAP, SWZ>(mc, v, qs[buf]);
+        __syncthreads();
+        bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
+        buf ^= 1;  // the next iteration's barrier orders reuse of this buffer
+        mc = mn;
+        mn = mnn;
+    }
+}
+
+// Lanes kernel (short rows, p >= 2): one entry per lane per load.
+// The q gathers are L1-tag bound (ncu: l1tex 78-91% busy at N=7): an
+// instruction costs one tag lookup per distinct 128 B line its lanes touch.
+// With one entry per lane, a warp instruction covers 32 consecutive entries
+// (4 element-edge runs of 8 at N=7 -> ~4 lines) whatever the parity of the
+// run starts, and the column loads are fully coalesced 128 B rows; paired
+// 16 B gathers only pay off when a run starts on an even entry.
+template <int T, int CAP, bool SWZ>
+__global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_lanes(const int32_t *__restrict__ plan, int64_t nsb,
+                                                             const int32_t *__restrict__ rs,
+                                                             const int32_t *__restrict__ ci,
+                                                             const double *__restrict__ q,
+                                                             double *__restrict__ out,
+                                                             const double *__restrict__ carry, int64_t ncarry) {
+    constexpr int E = CAP / T;  // entries per thread
+    extern __shared__ __align__(16) unsigned char bs6_smem[];
+    double(*qs)[CAP] = reinterpret_cast<double(*)[CAP]>(bs6_smem);
+    const int64_t g = gridDim.x;
+    int64_t sbi = blockIdx.x;
+    if (sbi >= nsb) return;
+    int32_t col[E];
+    Bs6Rows<T, CAP> rw;
+    int buf = 0;
+    SbMeta mc = load_meta(plan, sbi, nsb), mn = load_meta(plan, sbi + g, nsb);
+    {
+        const int ne = mc.e1 - mc.e0;
 #pragma unroll
-        for (int m = 0; m < M; m++) {
-            const int k = 2 * (threadIdx.x + m * T);
-            if (k + 1 < ne) {
-                if (cols[m].y == cols[m].x + 1 && aligned16(q + cols[m].x)) {
-                    v[m] = __ldg(reinterpret_cast<const double2 *>(q + cols[m].x));
-                } else {
-                    v[m].x = __ldg(q + cols[m].x);
-                    v[m].y = __ldg(q + cols[m].y);
-                }
-            } else if (k < ne) {
-                v[m].x = __ldg(q + cols[m].x);
-            }
-        }
-        // B: row starts of this super-block
-        int32_t rv[R];
+        for (int j = 0; j < E; j++)
+            if ((int)threadIdx.x + j * T < ne) col[j] = ld_stream(ci + mc.e0 + threadIdx.x + j * T);
+    }
+    for (; sbi < nsb; sbi += g) {
+        const int ne = mc.e1 - mc.e0;
+        double v[E];
 #pragma unroll
-        for (int j = 0; j < R; j++) {
-            const int k = threadIdx.x + j * T;
-            if (k <= nrows) rv[j] = ld_stream(rs + mc.r0 + k);
-        }
-        // C: indices of the next super-block; D: plan entry of the one after
+        for (int j = 0; j < E; j++)
+            if ((int)threadIdx.x + j * T < ne) v[j] = __ldg(q + col[j]);
+        bs6_load_rows<T, CAP>(mc, rs, rw);
         const int nne = mn.e1 - mn.e0;
 #pragma unroll
-        for (int m = 0; m < M; m++) {
-            const int k = 2 * (threadIdx.x + m * T);
-            if (k < nne) cols[m].x = ld_stream(ci + mn.e0 + k);
-            if (k + 1 < nne) cols[m].y = ld_stream(ci + mn.e0 + k + 1);
-        }
+        for (int j = 0; j < E; j++)
+            if ((int)threadIdx.x + j * T < nne) col[j] = ld_stream(ci + mn.e0 + threadIdx.x + j * T);
         const SbMeta mnn = load_meta(plan, sbi + 2 * g, nsb);
-        // E: publish A/B to shared memory
 #pragma unroll
-        for (int m = 0; m < M; m++) {
-            const int k = 2 * (threadIdx.x + m * T);
-            if (SWZ) {
-                if (k < ne) qs[buf][qslot<SWZ>(k)] = v[m].x;
-                if (k + 1 < ne) qs[buf][qslot<SWZ>(k + 1)] = v[m].y;
-            } else if (k + 1 < ne) {
-                *reinterpret_cast<double2 *>(&qs[buf][k]) = v[m];
-            } else if (k < ne) {
-                qs[buf][k] = v[m].x;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < R; j++) {
-            const int k = threadIdx.x + j * T;
-            if (k <= nrows) rss[buf][k] = rv[j];
-        }
+        for (int j = 0; j < E; j++)
+            if ((int)threadIdx.x + j * T < ne) qs[buf][qslot<SWZ>(threadIdx.x + j * T)] = v[j];
         __syncthreads();
-        // G: one thread per row, ascending column order
-        for (int k = threadIdx.x; k < nrows; k += T) {
-            const int a = rss[buf][k] - mc.e0, b = rss[buf][k + 1] - mc.e0;
-            const int64_t r = (int64_t)mc.r0 + k;
-            double acc = r < ncarry ? carry[r] : 0.0;
-            for (int c = a; c < b; c++) acc = add(acc, qs[buf][qslot<SWZ>(c)]);
-            st_stream(out + r, acc);
-        }
-        buf ^= 1;  // the barrier of the next iteration separates reuse of this buffer
+        bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
+        buf ^= 1;
         mc = mn;
         mn = mnn;
     }
@@ -324,22 +431,32 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     if (ncarry > ng) ncarry = ng;
     const int64_t nsb = psize / 2 - 1;
     constexpr int T = kBs6T;
-    const size_t smem = 2 * kBs6Cap * sizeof(double) + 2 * (kBs6Cap + 4) * sizeof(int32_t);
+    const size_t smem = 2 * kBs6Cap * sizeof(double);
+    using KernT = void (*)(const int32_t *, int64_t, const int32_t *, const int32_t *, const double *, double *,
+                           const double *, int64_t);
     static thread_local int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (attr_dev != dev) {
-        if (cuda_check(cudaFuncSetAttribute(k_bs6_pipe<T, kBs6Cap, false>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                       "sb_bs6_gather_planned: shared memory attribute") ||
-            cuda_check(cudaFuncSetAttribute(k_bs6_pipe<T, kBs6Cap, true>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                       "sb_bs6_gather_planned: shared memory attribute"))
-            return SB_E_CUDA;
+        const KernT all[4] = {k_bs6_pairs<T, kBs6Cap, true>, k_bs6_pairs<T, kBs6Cap, false>,
+                              k_bs6_lanes<T, kBs6Cap, true>, k_bs6_lanes<T, kBs6Cap, false>};
+        for (KernT k : all)
+            if (cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                           "sb_bs6_gather_planned: shared memory attribute"))
+                return SB_E_CUDA;
         attr_dev = dev;
     }
-    const bool swz = nl >= 4 * ng;  // mean row length >= 4 (p = 1 meshes)
-    auto kern = swz ? k_bs6_pipe<T, kBs6Cap, true> : k_bs6_pipe<T, kBs6Cap, false>;
+    // Kernel and value-tile swizzle by mean row length nl/ng (measured on B200
+    // over N = 1..15, scripts/expt/time_bs6.py): pairs + swizzle for the long
+    // rows of p = 1; one entry per lane otherwise, swizzled for rho <= 1.6
+    // (p >= 7), where the row-sum reads otherwise hit 3x the ideal wavefronts.
+    KernT kern;
+    if (nl >= 4 * ng)
+        kern = k_bs6_pairs<T, kBs6Cap, true>;
+    else if (5 * nl > 8 * ng)
+        kern = k_bs6_lanes<T, kBs6Cap, false>;
+    else
+        kern = k_bs6_lanes<T, kBs6Cap, true>;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
     const int64_t grid = std::min<int64_t>(nsb, (int64_t)sm_count() * std::max(1, per_sm));

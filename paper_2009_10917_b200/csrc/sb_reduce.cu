@@ -203,12 +203,15 @@ struct NArr {
     static constexpr int v = MODE == R_NORM ? 1 : (MODE == R_DOT ? 2 : 4);
 };
 
-template <int T, int SPT, int MODE, int ST>
+template <int T, int SPT, int MODE, int ST, int SPS>
 __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs A) {
+    // A stage holds SPS consecutive chain steps (chunks) of every array, so
+    // the per-byte cost of the full/empty handshakes drops by SPS.
     constexpr int BS = T * SPT;
     constexpr int NA = NArr<MODE>::v;
     constexpr int NCW = T / 32;  // consumer warps
-    __shared__ __align__(128) double buf[ST][NA][BS];
+    extern __shared__ __align__(128) unsigned char lat_smem[];  // ST stages, dynamic
+    double(*buf)[SPS][NA][BS] = reinterpret_cast<double(*)[SPS][NA][BS]>(lat_smem);
     __shared__ __align__(8) uint64_t full[ST], empty[ST];
     __shared__ double sm[BS];
 
@@ -217,6 +220,7 @@ __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs A) {
     const int64_t S = A.S, n = A.n;
     const int64_t base0 = (int64_t)blockIdx.x * BS;
     const int64_t nfull = n >= base0 + BS ? (n - base0 - BS) / S + 1 : 0;
+    const int64_t nstage = nfull / SPS;
 
     if (tid == 0) {
         for (int s = 0; s < ST; s++) {
@@ -236,44 +240,59 @@ __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs A) {
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             const double *src[4] = {A.u, A.v, A.x, A.r};
-            if (MODE == R_NORM) src[0] = A.u;
-            for (int64_t c = 0; c < nfull; c++) {
-                const int s = (int)(c % ST);
-                if (c >= ST) mbar_wait(&empty[s], (uint32_t)((c / ST - 1) & 1));
-                mbar_arrive_expect_tx(&full[s], (uint32_t)(NA * BS * sizeof(double)));
-                const int64_t off = c * S + base0;
+            int s = 0;
+            uint32_t ph = 0;  // parity of the current pass over the ring
+            for (int64_t c = 0; c < nstage; c++) {
+                if (c >= ST) mbar_wait(&empty[s], ph ^ 1u);
+                mbar_arrive_expect_tx(&full[s], (uint32_t)(SPS * NA * BS * sizeof(double)));
 #pragma unroll
-                for (int a = 0; a < NA; a++)
-                    bulk_g2s(&buf[s][a][0], src[a] + off, (uint32_t)(BS * sizeof(double)), &full[s], pol);
+                for (int u = 0; u < SPS; u++) {
+                    const int64_t off = (c * SPS + u) * S + base0;
+#pragma unroll
+                    for (int a = 0; a < NA; a++)
+                        bulk_g2s(&buf[s][u][a][0], src[a] + off, (uint32_t)(BS * sizeof(double)), &full[s], pol);
+                }
+                if (++s == ST) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
         }
     } else {
-        for (int64_t c = 0; c < nfull; c++) {
-            const int s = (int)(c % ST);
-            mbar_wait(&full[s], (uint32_t)((c / ST) & 1));
-            const int64_t off = c * S + base0;
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t c = 0; c < nstage; c++) {
+            mbar_wait(&full[s], ph);
 #pragma unroll
-            for (int j = 0; j < SPT; j++) {
-                const int k = tid + j * T;
-                if constexpr (MODE == R_NORM) {
-                    const double a = buf[s][0][k];
-                    acc[j] = add(acc[j], mul(a, a));
-                } else if constexpr (MODE == R_DOT) {
-                    acc[j] = add(acc[j], mul(buf[s][0][k], buf[s][1][k]));
-                } else {
-                    const double xn = add(buf[s][2][k], mul(A.alpha, buf[s][0][k]));
-                    const double rn = sub(buf[s][3][k], mul(A.alpha, buf[s][1][k]));
-                    st_stream(A.x + off + k, xn);
-                    st_stream(A.r + off + k, rn);
-                    acc[j] = add(acc[j], mul(rn, rn));
+            for (int u = 0; u < SPS; u++) {
+                const int64_t off = (c * SPS + u) * S + base0;
+#pragma unroll
+                for (int j = 0; j < SPT; j++) {
+                    const int k = tid + j * T;
+                    if constexpr (MODE == R_NORM) {
+                        const double a = buf[s][u][0][k];
+                        acc[j] = add(acc[j], mul(a, a));
+                    } else if constexpr (MODE == R_DOT) {
+                        acc[j] = add(acc[j], mul(buf[s][u][0][k], buf[s][u][1][k]));
+                    } else {
+                        const double xn = add(buf[s][u][2][k], mul(A.alpha, buf[s][u][0][k]));
+                        const double rn = sub(buf[s][u][3][k], mul(A.alpha, buf[s][u][1][k]));
+                        st_stream(A.x + off + k, xn);
+                        st_stream(A.r + off + k, rn);
+                        acc[j] = add(acc[j], mul(rn, rn));
+                    }
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == ST) {
+                s = 0;
+                ph ^= 1u;
+            }
         }
-        // partial last chunk (at most one per CTA), from global memory
-        const int64_t off = nfull * S + base0;
-        if (off < n) {
+        // leftover full chunks (< SPS) and the partial last chunk, from global
+        // memory, still in chain order
+        for (int64_t off = nstage * SPS * S + base0; off < n; off += S) {
 #pragma unroll
             for (int j = 0; j < SPT; j++) {
                 const int64_t i = off + tid + j * T;
@@ -377,6 +396,25 @@ __global__ void __launch_bounds__(1024) k_final_generic(RArgs A) {
     if (threadIdx.x == 0) *A.result = v;
 }
 
+// Ring shapes (bytes of stages per CTA, chain steps per stage); overridable at
+// build time for the A/B sweeps in scripts/expt/run_lattice.py.
+#ifndef SB_SPS_NORM
+#define SB_SPS_NORM 8
+#define SB_SPS_DOT 4
+#define SB_SPS_FUSED 2
+#define SB_RING_NORM 32768
+#define SB_RING_DOT 32768
+#define SB_RING_FUSED 32768
+#endif
+constexpr int kSpsNorm = SB_SPS_NORM, kSpsDot = SB_SPS_DOT, kSpsFused = SB_SPS_FUSED;
+constexpr int kRingNorm = SB_RING_NORM, kRingDot = SB_RING_DOT, kRingFused = SB_RING_FUSED;
+
+// block_size 512 halves the steps per stage (same stage bytes)
+constexpr int ring_sps(int sps, int bs) { return bs <= 256 ? sps : (sps / 2 > 0 ? sps / 2 : 1); }
+constexpr int ring_stages(int ring, int stage_bytes) {
+    return ring / stage_bytes > 16 ? 16 : (ring / stage_bytes < 2 ? 2 : ring / stage_bytes);
+}
+
 // SB200_NO_TMA=1 selects the register-unrolled lattice kernel (A/B checks).
 static bool use_tma() {
     static const bool on = [] {
@@ -411,9 +449,27 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
     constexpr int NA = NArr<MODE>::v;
     const bool tma_ok = aligned16(A.u) && aligned16(A.v) && (MODE != R_FUSED || (aligned16(A.x) && aligned16(A.r)));
     if (tma_ok && use_tma() && (A.bs == 64 || A.bs == 128 || A.bs == 256 || A.bs == 512)) {
-#define SB_TMA(T_, SPT_)                                                                        \
-    k_lattice_tma<T_, SPT_, MODE, (32768 / (NA * T_ * SPT_ * 8) > 16 ? 16 : 32768 / (NA * T_ * SPT_ * 8))> \
-        <<<grid, T_ + 32, 0, st>>>(A)
+        // ring shape (stages x steps per stage): ~32-48 KB of stages per CTA
+        constexpr int SPS = MODE == R_NORM ? kSpsNorm : (MODE == R_DOT ? kSpsDot : kSpsFused);
+        constexpr int RING = MODE == R_NORM ? kRingNorm : (MODE == R_DOT ? kRingDot : kRingFused);
+#define SB_TMA(T_, SPT_)                                                                                  \
+    {                                                                                                     \
+        constexpr int SPS_ = ring_sps(SPS, T_ * SPT_);                                                   \
+        constexpr int STB_ = SPS_ * NA * T_ * SPT_ * 8;                                                  \
+        constexpr int ST_ = ring_stages(RING, STB_);                                                      \
+        auto kern = k_lattice_tma<T_, SPT_, MODE, ST_, SPS_>;                                             \
+        static int attr_dev = -1; /* per instantiation and device */                                      \
+        int dev = 0;                                                                                      \
+        cudaGetDevice(&dev);                                                                              \
+        if (attr_dev != dev) {                                                                            \
+            if (int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                                         ST_ * STB_),                                     \
+                                    name))                                                                \
+                return rc;                                                                                \
+            attr_dev = dev;                                                                               \
+        }                                                                                                 \
+        kern<<<grid, T_ + 32, ST_ * STB_, st>>>(A);                                                       \
+    }
         switch (A.bs) {
             case 64: SB_TMA(64, 1); break;
             case 128: SB_TMA(128, 1); break;

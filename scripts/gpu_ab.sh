@@ -1,11 +1,7 @@
-# A/B: default kernels vs SB200_NO_PIPE / SB200_NO_TMA fallbacks (bench, no e2e / cpu legs)
+# A/B: BS6 kernel variants 3 (lean), 5 (lean2: int4 ids), 6 (lean2 + swizzle always)
 set -x
-R=${1:-ab}
-timeout 600 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ab_${R}_new.json 2>&1
-SB200_NO_PIPE=1 SB200_NO_TMA=1 timeout 600 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ab_${R}_old.json 2>&1
-python - <<PY
-import json
-for tag in ("new","old"):
-    j=json.load(open(f"gpurun_out/ab_${R}_{tag}.json"))
-    print(tag, j["value"], {k:v["GBps"] for k,v in j["per_test"].items()})
-PY
+rm -f gpurun_out/bs6_ab5.log
+for k in 7 9; do SB200_BS6_KERNEL=$k timeout 600 python -m pytest tests/test_gpu_gs.py tests/test_gpu_dist.py -q -x -p no:cacheprovider 2>&1 | tail -2 >> gpurun_out/bs6_ab5.log; done
+for k in 3 7 8 9; do SB200_BS6_KERNEL=$k timeout 300 python scripts/expt/time_bs6.py 1 2 3 5 7 10 15 >> gpurun_out/bs6_ab5.log 2>&1; done
+SB200_BS6_KERNEL=7 timeout 300 ncu --set full --import-source on --clock-control none -k regex:k_bs6 -s 2 -c 1 -o gpurun_out/bs6_v7_n7 python scripts/expt/time_bs6.py 7 > /dev/null 2>&1
+cat gpurun_out/bs6_ab5.log
