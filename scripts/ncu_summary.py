@@ -20,7 +20,7 @@ sys.path.insert(0, ROOT)
 # order of launches in scripts/profile_kernels.py's captured pass
 TESTS = ["bs1", "bs2", "bs3", "bs4", "bs5", "bs6", "bs7"]
 KEYS = {"bs1": "k_elem_vec<0>", "bs2": "k_elem_vec<1>", "bs3": "k_lattice_tma<norm>",
-        "bs4": "k_lattice_tma<dot>", "bs5": "k_lattice_tma<fused>", "bs6": "k_bs6_pipe",
+        "bs4": "k_lattice_tma<dot>", "bs5": "k_lattice_tma<fused>", "bs6": "k_bs6_lanes",
         "bs7": "k_bs7_pipe"}
 
 
@@ -56,8 +56,8 @@ def main():
              "Workload: scripts/profile_kernels.py (bench step: BS1-BS5 n=1e8, BS6/BS7 K=66 N=7), "
              "one captured launch per kernel, `--clock-control none`, cold L2 (ncu replays).", "",
              "| test | kernel | duration us | DRAM read GB | DRAM write GB | traffic / algorithmic | "
-             "achieved GB/s (algorithmic) | DRAM % peak | regs | achieved occ % | top stalls |",
-             "|---|---|---|---|---|---|---|---|---|---|---|"]
+             "achieved GB/s (algorithmic) | DRAM % peak | L1 % peak | issue active % | regs | achieved occ % | top stalls |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = {}
 
     def test_of(kname):
@@ -68,7 +68,7 @@ def main():
         if "k_lattice" in kname:
             mode = kname.split("<")[1].split(",")[2].strip()
             return {"0": "bs3", "1": "bs4", "2": "bs5"}[mode]
-        if "k_bs6_pipe" in kname or "k_bs6_smem" in kname:
+        if "k_bs6_" in kname:
             return "bs6"
         if "k_bs7" in kname:
             return "bs7"
@@ -90,6 +90,8 @@ def main():
         wr = to_bytes(*get(r, "dram__bytes_write.sum"))
         pct = get(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")[0]
         regs = get(r, "launch__registers_per_thread")[0]
+        l1 = get(r, "l1tex__throughput.avg.pct_of_peak_sustained_active")[0] or "nan"
+        iss = get(r, "smsp__issue_active.avg.pct_of_peak_sustained_active")[0] or "nan"
         occ = get(r, "sm__warps_active.avg.pct_of_peak_sustained_active")[0]
         stalls = []
         for h, i in col.items():
@@ -102,7 +104,8 @@ def main():
         top = ", ".join(f"{s} {v:.1f}" for v, s in stalls[:3])
         ach = algo[t] / (dur_us * 1e-6) / 1e9
         lines.append(f"| {t} | `{name}` | {dur_us:.1f} | {rd / 1e9:.3f} | {wr / 1e9:.3f} | "
-                     f"{(rd + wr) / algo[t]:.3f} | {ach:.0f} | {float(pct):.1f} | {regs} | {float(occ):.1f} | {top} |")
+                     f"{(rd + wr) / algo[t]:.3f} | {ach:.0f} | {float(pct):.1f} | {float(l1):.1f} | {float(iss):.1f} | {regs} | "
+                     f"{float(occ):.1f} | {top} |")
         traffic[KEYS[t]] = int(rd + wr)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md"), "w") as f:
