@@ -189,6 +189,47 @@ int sb_ids_minmax(const int32_t *ids, int64_t n, int32_t *out, sb_stream_t strea
 int sb_dot_compensated(const double *u, const double *v, int64_t n, void *workspace,
                        double *result, sb_stream_t stream);
 
+
+/* ---- device-resident CG (cg.py:27-72) -----------------
+ * The solver's scalars live in device memory: alpha = rr / pAp and
+ * beta = rr_new / rr are formed by one-thread control kernels (IEEE
+ * division, exactly as Python's) and read by the streaming kernels, so no
+ * host sync is needed per iteration.  All kernels are gated
+ * on `active`; launching more iterations than needed is harmless.  One
+ * iteration, given ap = A p computed by the caller on the same stream:
+ *     sb_cg_pap(p, ap, ...); sb_cg_update(fused, p, ap, x, r, ...);
+ *     sb_cg_direction(r, p, ...);
+ * Iterates, iteration count and final r.r are bitwise those of cg_solve with
+ * host scalars for the same ReductionConfig. */
+enum { SB_CG_RUNNING = 0, SB_CG_CONVERGED = 1, SB_CG_EXHAUSTED = 2, SB_CG_NOT_SPD = 3 };
+typedef struct sb_cg_state {
+    double rr;          /* r.r of the current iterate */
+    double rr_new;      /* r.r after the update */
+    double pap;         /* p.Ap of the current direction */
+    double tol;         /* eps, or eps * b.b for a relative tolerance */
+    double fail_pap;    /* p.Ap that stopped the solve (SB_CG_NOT_SPD) */
+    double alpha;       /* rr / pAp of the current iteration */
+    double beta;        /* rr_new / rr of the current iteration */
+    int64_t iterations; /* completed iterations */
+    int64_t max_iter;
+    int32_t active;     /* 1 while iterating */
+    int32_t status;     /* SB_CG_* */
+} sb_cg_state;
+
+/* rr0 = r0.r0 (device), bb = b.b (device) for a relative tolerance or NULL. */
+int sb_cg_begin(sb_cg_state *state, const double *rr0, const double *bb, double eps,
+                int64_t max_iter, sb_stream_t stream);
+/* kernels.py:111 bs4_dot(p, ap) -> state->pap, then the cg.py:61-64 SPD check. */
+int sb_cg_pap(const double *p, const double *ap, int64_t n, int64_t block_size,
+              int64_t n_blocks, void *workspace, sb_cg_state *state, sb_stream_t stream);
+/* cg.py:65-70: fused (BS5) or unfused (BS2, BS2, BS3) update of x and r. */
+int sb_cg_update(int fused, const double *p, const double *ap, double *x, double *r,
+                 int64_t n, int64_t block_size, int64_t n_blocks, void *workspace,
+                 sb_cg_state *state, sb_stream_t stream);
+/* cg.py:71-74: p = r + beta p, then advance the iteration. */
+int sb_cg_direction(const double *r, double *p, int64_t n, sb_cg_state *state,
+                    sb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

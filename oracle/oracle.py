@@ -141,6 +141,39 @@ def bs5_fused_cg_update(alpha, p, ap, x, r, block_size=256, n_blocks=512) -> flo
     return out.value
 
 
+def cg_solve_diag(d, b, x0, eps, max_iter, block_size=256, n_blocks=512, fused=True, relative=False):
+    """cg.py:27-72 with cg.py:75-82's diagonal operator (A v = d * v), on the
+    kernels above.  Returns (x, iterations, final_rr, converged) or raises
+    ValueError("not SPD ...") where the reference raises NotSPDError."""
+    if eps <= 0:
+        raise ValueError(f"eps must be positive, got {eps}")
+    d, b = _f64(d), _f64(b)
+    x = _f64(x0).copy()
+    r = b.copy()
+    bs2_axpy(-1.0, d * x, 1.0, r)
+    p = r.copy()
+    rr = bs3_norm2(r, block_size, n_blocks)
+    tol = eps * bs3_norm2(b, block_size, n_blocks) if relative else eps
+    it = 0
+    while rr > tol and it < max_iter:
+        ap = d * p
+        pap = bs4_dot(p, ap, block_size, n_blocks)
+        if pap <= 0.0:
+            raise ValueError(f"not SPD: p . Ap = {pap} at iteration {it}")
+        alpha = rr / pap
+        if fused:
+            rr_new = bs5_fused_cg_update(alpha, p, ap, x, r, block_size, n_blocks)
+        else:
+            bs2_axpy(alpha, p, 1.0, x)
+            bs2_axpy(-alpha, ap, 1.0, r)
+            rr_new = bs3_norm2(r, block_size, n_blocks)
+        beta = rr_new / rr
+        bs2_axpy(1.0, r, beta, p)
+        rr = rr_new
+        it += 1
+    return x, it, rr, rr <= tol
+
+
 # --- exact references (reference.py) ---------------------------------------
 
 def fsum_norm2(x) -> float:

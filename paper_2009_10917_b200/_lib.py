@@ -63,6 +63,11 @@ _SIGS = {
                                          _c_vp]),
     "sb_histogram": (_c_int, [_c_vp, _c_i64, _c_i64, _c_vp, _c_vp]),
     "sb_bs6_plan_size": (_c_i64, [_c_i64, _c_i64]),
+    "sb_cg_begin": (_c_int, [_c_vp, _c_vp, _c_vp, _c_dbl, _c_i64, _c_vp]),
+    "sb_cg_pap": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp]),
+    "sb_cg_update": (_c_int, [_c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp,
+                              _c_vp]),
+    "sb_cg_direction": (_c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_vp]),
     "sb_bs6_make_plan": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_vp]),
     "sb_bs6_gather_planned": (_c_int, [_c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp,
                                        _c_vp, _c_vp, _c_i64, _c_vp]),

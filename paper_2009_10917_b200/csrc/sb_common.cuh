@@ -38,6 +38,26 @@ __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, 
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
 
+// ---- device-resident scalars (device CG, cg.py:27-72 with alpha/beta on
+// the GPU): value = scale * (*ptr) when ptr is set, else scale; scale is +-1,
+// an exact multiply.  (The divisions forming alpha and beta run in the tiny
+// sb_cg.cu control kernels, so the streaming kernels stay DFMA-free.)
+struct DevCoef {
+    const double *ptr;
+    double scale;
+};
+__device__ __forceinline__ double coef_value(const DevCoef &c) {
+    return c.ptr ? __dmul_rn(c.scale, *c.ptr) : c.scale;
+}
+
+// Gated variants used by the device CG (sb_cg.cu): every CTA returns at once
+// when *gate == 0, so a converged solve turns later iterations into no-ops.
+int cg_axpy(const double *x, double *y, int64_t n, DevCoef a, DevCoef b, const int32_t *gate,
+            cudaStream_t st, const char *name);
+int cg_reduce(int mode, const double *u, const double *v, double *x, double *r, int64_t n, int64_t bs,
+              int64_t nb, void *ws, double *result, const int32_t *gate, const double *alpha,
+              cudaStream_t st, const char *name);
+
 // ---- cache-policy helpers: HBM streams are touched once -> evict-first.
 __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ld_stream(const double2 *p) { return __ldcs(p); }

@@ -43,7 +43,17 @@ struct RArgs {
     unsigned *ticket;
     double *result;
     double *lattice;  // generic path only
+    // device CG: *gate == 0 -> every CTA returns; alpha read from *alpha_ptr
+    const int32_t *gate;
+    const double *alpha_ptr;
 };
+
+// Gate check + device alpha at kernel entry (a no-op for plain calls).
+__device__ __forceinline__ bool resolve(RArgs &A) {
+    if (A.gate && *A.gate == 0) return false;
+    if (A.alpha_ptr) A.alpha = *A.alpha_ptr;
+    return true;
+}
 
 // Workspace layout: [ticket: 256 B][partials: nb doubles][generic: S + bs doubles]
 static size_t ws_bytes(int64_t bs, int64_t nb) {
@@ -144,7 +154,9 @@ __device__ __forceinline__ void second_stage(const RArgs &A, double *sm, int bs,
 }
 
 template <int T, int SPT, int MODE, int U>
-__global__ void __launch_bounds__(T, (1024 / T) < 32 ? (1024 / T) : 32) k_lattice(RArgs A) {
+__global__ void __launch_bounds__(T, (1024 / T) < 32 ? (1024 / T) : 32) k_lattice(RArgs Ain) {
+    RArgs A = Ain;
+    if (!resolve(A)) return;
     __shared__ double sm[T * SPT];
     const int bs = T * SPT;
     const int64_t slot0 = (int64_t)blockIdx.x * bs + threadIdx.x;
@@ -204,7 +216,9 @@ struct NArr {
 };
 
 template <int T, int SPT, int MODE, int ST, int SPS>
-__global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs A) {
+__global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs Ain) {
+    RArgs A = Ain;
+    if (!resolve(A)) return;
     // A stage holds SPS consecutive chain steps (chunks) of every array, so
     // the per-byte cost of the full/empty handshakes drops by SPS.
     constexpr int BS = T * SPT;
@@ -357,7 +371,9 @@ __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs A) {
 
 // ---- generic path (block_size > 1024): lattice in global memory ----------
 template <int MODE>
-__global__ void __launch_bounds__(256) k_lattice_global(RArgs A) {
+__global__ void __launch_bounds__(256) k_lattice_global(RArgs Ain) {
+    RArgs A = Ain;
+    if (!resolve(A)) return;
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < A.S;
          s += (int64_t)gridDim.x * blockDim.x) {
         double acc = 0.0;
@@ -380,11 +396,13 @@ __device__ double fold_global_row(double *row, int64_t bs) {
 }
 
 __global__ void __launch_bounds__(1024) k_fold_blocks(RArgs A) {
+    if (A.gate && *A.gate == 0) return;
     const double v = fold_global_row(A.lattice + (int64_t)blockIdx.x * A.bs, A.bs);
     if (threadIdx.x == 0) A.partials[blockIdx.x] = v;
 }
 
 __global__ void __launch_bounds__(1024) k_final_generic(RArgs A) {
+    if (A.gate && *A.gate == 0) return;
     double *srow = A.lattice + A.S;  // bs scratch doubles
     for (int64_t t = threadIdx.x; t < A.bs; t += blockDim.x) {
         double acc = 0.0;
@@ -504,6 +522,23 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
     }
 #undef SB_LAT
     return launch_check(name);
+}
+
+int cg_reduce(int mode, const double *u, const double *v, double *x, double *r, int64_t n, int64_t bs,
+              int64_t nb, void *ws, double *result, const int32_t *gate, const double *alpha,
+              cudaStream_t st, const char *name) {
+    RArgs A{};
+    A.u = u; A.v = v; A.x = x; A.r = r; A.n = n; A.bs = bs; A.nb = nb; A.result = result;
+    A.gate = gate; A.alpha_ptr = alpha;
+    if (!gate || (n > 0 && (!u || !v || (mode == R_FUSED && (!x || !r || !alpha))))) {
+        set_error("%s: invalid arguments", name);
+        return SB_E_INVALID;
+    }
+    switch (mode) {
+        case R_NORM: return launch_reduce<R_NORM>(A, ws, st, name);
+        case R_DOT: return launch_reduce<R_DOT>(A, ws, st, name);
+        default: return launch_reduce<R_FUSED>(A, ws, st, name);
+    }
 }
 
 // ---- validators / helpers ------------------------------------------------

@@ -44,10 +44,20 @@ __device__ __forceinline__ double elem(double alpha, double x, double beta, doub
     return add(mul(alpha, x), mul(beta, y));
 }
 
-template <int OP, int U, int T>
+struct ElemDev {
+    DevCoef a, b;
+    const int32_t *gate;
+};
+
+template <int OP, int U, int T, bool DEV = false>
 __global__ void __launch_bounds__(T) k_elem_vec(const double2 *x, double2 *y, int64_t n2, double alpha,
                                                double beta, const double *xs, double *ys,
-                                               int64_t head_idx, int64_t tail_idx) {
+                                               int64_t head_idx, int64_t tail_idx, ElemDev dv = {}) {
+    if (DEV) {
+        if (*dv.gate == 0) return;
+        alpha = coef_value(dv.a);
+        beta = coef_value(dv.b);
+    }
     const int64_t base = (int64_t)blockIdx.x * (T * U) + threadIdx.x;
     double2 xv[U], yv[U];
 #pragma unroll
@@ -79,17 +89,22 @@ __global__ void __launch_bounds__(T) k_elem_vec(const double2 *x, double2 *y, in
 }
 
 // Fallback when x and y are not co-aligned to 16 B: scalar grid-stride.
-template <int OP>
+template <int OP, bool DEV = false>
 __global__ void __launch_bounds__(256) k_elem_scalar(const double *x, double *y, int64_t n, double alpha,
-                                                    double beta) {
+                                                    double beta, ElemDev dv = {}) {
+    if (DEV) {
+        if (*dv.gate == 0) return;
+        alpha = coef_value(dv.a);
+        beta = coef_value(dv.b);
+    }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         y[i] = elem<OP>(alpha, x[i], beta, y[i]);
 }
 
-template <int OP>
+template <int OP, bool DEV = false>
 static int launch_elem(const double *x, double *y, int64_t n, double alpha, double beta,
-                       cudaStream_t st, const char *name) {
+                       cudaStream_t st, const char *name, ElemDev dv = {}) {
     clear_error();
     if (n < 0 || ((x == nullptr || y == nullptr) && n > 0)) {
         set_error("%s: invalid arguments (n=%lld)", name, (long long)n);
@@ -99,7 +114,7 @@ static int launch_elem(const double *x, double *y, int64_t n, double alpha, doub
     const uintptr_t ax = reinterpret_cast<uintptr_t>(x) & 15u, ay = reinterpret_cast<uintptr_t>(y) & 15u;
     if (ax != ay || (ax & 7u)) {
         const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
-        k_elem_scalar<OP><<<blocks, 256, 0, st>>>(x, y, n, alpha, beta);
+        k_elem_scalar<OP, DEV><<<blocks, 256, 0, st>>>(x, y, n, alpha, beta, dv);
         return launch_check(name);
     }
     const int64_t head = ax ? 1 : 0;
@@ -107,10 +122,19 @@ static int launch_elem(const double *x, double *y, int64_t n, double alpha, doub
     const int64_t tail = head + 2 * n2 < n ? head + 2 * n2 : -1;
     constexpr int T = 256, U = 4;
     const int64_t blocks = std::max<int64_t>(1, (n2 + (int64_t)T * U - 1) / ((int64_t)T * U));
-    k_elem_vec<OP, U, T><<<(unsigned)blocks, T, 0, st>>>(
+    k_elem_vec<OP, U, T, DEV><<<(unsigned)blocks, T, 0, st>>>(
         reinterpret_cast<const double2 *>(x + head), reinterpret_cast<double2 *>(y + head), n2, alpha,
-        beta, x, y, head ? 0 : -1, tail);
+        beta, x, y, head ? 0 : -1, tail, dv);
     return launch_check(name);
+}
+
+int cg_axpy(const double *x, double *y, int64_t n, DevCoef a, DevCoef b, const int32_t *gate,
+            cudaStream_t st, const char *name) {
+    if (!gate) {
+        set_error("%s: null gate", name);
+        return SB_E_INVALID;
+    }
+    return launch_elem<OP_AXPY, true>(x, y, n, 0.0, 0.0, st, name, ElemDev{a, b, gate});
 }
 
 }  // namespace sb

@@ -208,6 +208,33 @@ def main() -> None:
                              "trials": s.trials})
     G["csv_header"] = cli.CSV_HEADER
 
+    # ---- CG (cg.py:27-72) on diagonal operators: elementwise d*v rounds the
+    # same on every device, so these pin the device CG bitwise -------------
+    from streambench import cg as rcg
+    G["cg"] = []
+    cases = [  # n, seed, d range, eps, max_iter, cfg, fused, relative, x0 nonzero
+        (1000, 1, (1.0, 10.0), 1e-20, 200, (256, 512), True, False, False),
+        (1000, 1, (1.0, 10.0), 1e-20, 200, (256, 512), False, False, False),
+        (4097, 2, (0.5, 50.0), 1e-18, 300, (64, 7), True, True, False),
+        (4097, 2, (0.5, 50.0), 1e-18, 300, (64, 7), False, True, True),
+        (3000, 3, (1.0, 1e4), 1e-30, 5, (256, 512), True, False, True),   # max_iter exhausted
+        (777, 4, (2.0, 2.0), 1e-20, 50, (32, 3), True, False, False),     # one distinct eigenvalue
+        (50000, 5, (1.0, 100.0), 1e-16, 400, (256, 512), True, True, True),
+    ]
+    for n, seed, (lo, hi), eps, mi, cfg, fused, rel, x0nz in cases:
+        rng = np.random.default_rng([seed, n, 77])
+        d = rng.uniform(lo, hi, n)
+        b = rng.uniform(-1, 1, n)
+        x0 = rng.uniform(-1, 1, n) if x0nz else np.zeros(n)
+        res = rcg.cg_solve(rcg.diagonal_operator(d), b, x0, eps, mi,
+                           kernels.ReductionConfig(*cfg), fused=fused, relative=rel)
+        G["cg"].append({"n": n, "seed": [seed, n, 77], "draws": "d~U(lo,hi);b~U(-1,1);x0~U(-1,1)|0",
+                        "d_range": [lo, hi], "eps": fx(eps), "max_iter": mi, "cfg": list(cfg),
+                        "fused": fused, "relative": rel, "x0_nonzero": x0nz,
+                        "in_hash": h(np.concatenate([d, b, x0])), "iterations": res.iterations,
+                        "final_rr": fx(res.final_rr), "converged": bool(res.converged),
+                        "x_hash": h(res.x)})
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(G, f, indent=1, sort_keys=True)
     np.savez_compressed(os.path.join(HERE, "arrays.npz"), **arrays)

@@ -65,3 +65,15 @@ def mesh_q_local(K, p, nl):
 
 def mesh_q_global(K, p, ng):
     return np.random.default_rng([0, K, p]).uniform(-1, 1, ng)
+
+
+def cg_inputs(rec):
+    """golden 'cg' records: rng(seed); d ~ U(lo, hi); b ~ U(-1, 1); x0 ~ U(-1, 1) or 0."""
+    n = rec["n"]
+    rng = np.random.default_rng(rec["seed"])
+    lo, hi = rec["d_range"]
+    d = rng.uniform(lo, hi, n)
+    b = rng.uniform(-1, 1, n)
+    x0 = rng.uniform(-1, 1, n) if rec["x0_nonzero"] else np.zeros(n)
+    assert sha(np.concatenate([d, b, x0])) == rec["in_hash"], "numpy stream changed"
+    return d, b, x0

@@ -226,7 +226,19 @@ def test_library_is_sm100a():
     assert "sm_100a" in out.stdout
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH],
                           capture_output=True, text=True).stdout
-    assert "DFMA" not in sass, "fp64 FMA contraction would break bitwise parity"
+    # DFMA is allowed only inside the device-CG control kernels, whose IEEE
+    # division (alpha = rr/pAp, beta = rr_new/rr) is a correctly rounded
+    # DFMA Newton sequence; every streaming kernel must be contraction-free.
+    funcs, cur = {}, None
+    for ln in sass.splitlines():
+        if "Function :" in ln:
+            cur = ln.split("Function :")[1].strip()
+            funcs[cur] = []
+        elif cur is not None:
+            funcs[cur].append(ln)
+    with_dfma = sorted(f for f, body in funcs.items() if any("DFMA" in x for x in body))
+    assert funcs, "no SASS functions found"
+    assert all("k_cg_check" in f or "k_cg_beta" in f for f in with_dfma), with_dfma
 
 
 def test_kernel_calls_fail_loudly_without_gpu():

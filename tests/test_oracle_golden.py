@@ -150,3 +150,17 @@ def test_carry_composition_bitexact(oracle):
                 acc += q[ci[c]]
         out_up[k] = acc
     assert np.array_equal(out_up, full[c_if * plane:])
+
+
+# --- cg.py:27-72 (diagonal operators; tests/golden 'cg' records) -------------
+
+def test_oracle_cg_matches_reference_golden(golden, oracle):
+    from goldens import cg_inputs
+    for rec in golden["cg"]:
+        d, b, x0 = cg_inputs(rec)
+        x, it, rr, conv = oracle.cg_solve_diag(d, b, x0, float.fromhex(rec["eps"]), rec["max_iter"],
+                                          *rec["cfg"], fused=rec["fused"], relative=rec["relative"])
+        assert it == rec["iterations"], rec
+        assert rr.hex() == rec["final_rr"], rec
+        assert conv == rec["converged"]
+        assert sha(x) == rec["x_hash"], rec
