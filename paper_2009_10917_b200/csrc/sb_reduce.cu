@@ -27,6 +27,19 @@
 
 namespace sb {
 
+// Ring shapes (bytes of stages per CTA, chain steps per stage); overridable at
+// build time for the A/B sweeps in scripts/expt/run_lattice.py.
+#ifndef SB_SPS_NORM
+#define SB_SPS_NORM 8
+#define SB_SPS_DOT 4
+#define SB_SPS_FUSED 2
+#define SB_RING_NORM 32768
+#define SB_RING_DOT 32768
+#define SB_RING_FUSED 32768
+#endif
+constexpr int kSpsNorm = SB_SPS_NORM, kSpsDot = SB_SPS_DOT, kSpsFused = SB_SPS_FUSED;
+constexpr int kRingNorm = SB_RING_NORM, kRingDot = SB_RING_DOT, kRingFused = SB_RING_FUSED;
+
 enum RMode { R_NORM = 0, R_DOT = 1, R_FUSED = 2 };
 
 struct RArgs {
@@ -413,19 +426,6 @@ __global__ void __launch_bounds__(1024) k_final_generic(RArgs A) {
     const double v = fold_global_row(srow, A.bs);
     if (threadIdx.x == 0) *A.result = v;
 }
-
-// Ring shapes (bytes of stages per CTA, chain steps per stage); overridable at
-// build time for the A/B sweeps in scripts/expt/run_lattice.py.
-#ifndef SB_SPS_NORM
-#define SB_SPS_NORM 8
-#define SB_SPS_DOT 4
-#define SB_SPS_FUSED 2
-#define SB_RING_NORM 32768
-#define SB_RING_DOT 32768
-#define SB_RING_FUSED 32768
-#endif
-constexpr int kSpsNorm = SB_SPS_NORM, kSpsDot = SB_SPS_DOT, kSpsFused = SB_SPS_FUSED;
-constexpr int kRingNorm = SB_RING_NORM, kRingDot = SB_RING_DOT, kRingFused = SB_RING_FUSED;
 
 // block_size 512 halves the steps per stage (same stage bytes)
 constexpr int ring_sps(int sps, int bs) { return bs <= 256 ? sps : (sps / 2 > 0 ? sps / 2 : 1); }

@@ -19,8 +19,8 @@ for so in sorted(glob.glob(os.path.join(HERE, "_lat", "*.so"))):
     libs[os.path.basename(so)[:-3]] = L
 
 dev = torch.device("cuda", 0)
-bs, nb = 256, 512
-for n in [int(float(a)) for a in (sys.argv[1:] or ["1e8", "4e8"])]:
+cfgs = [tuple(int(v) for v in c.split(",")) for c in os.environ.get("SB_CFGS", "256,512").split(";")]
+for (bs, nb), n in [(c, int(float(a))) for c in cfgs for a in (sys.argv[1:] or ["1e8", "4e8"])]:
     g = torch.Generator(device=dev).manual_seed(1)
     x, y, p, ap = (torch.rand(n, dtype=torch.float64, device=dev, generator=g) for _ in range(4))
     x0, r0 = x.clone(), y.clone()
@@ -55,6 +55,6 @@ for n in [int(float(a)) for a in (sys.argv[1:] or ["1e8", "4e8"])]:
             e1.synchronize()
             ms = e0.elapsed_time(e1) / reps
             line.append(f"{t} {nbytes / ms / 1e6:6.0f} GB/s{'' if ok else ' MISMATCH'}")
-        print(f"n={n:.0e} {name}: " + " | ".join(line), flush=True)
+        print(f"n={n:.0e} cfg=({bs},{nb}) {name}: " + " | ".join(line), flush=True)
     del x, y, p, ap, x0, r0
     torch.cuda.empty_cache()
