@@ -444,7 +444,7 @@ def traffic_from_profiles(kernel_key):
 
 KERNEL_KEYS = {"bs1": "k_elem_vec<0>", "bs2": "k_elem_vec<1>", "bs3": "k_lattice_tma<norm>",
                "bs4": "k_lattice_tma<dot>", "bs5": "k_lattice_tma<fused>", "bs6": "k_bs6_lanes",
-               "bs7": "k_bs7_pipe"}
+               "bs7": "k_bs7_lanes"}
 
 
 def main_ours(args):

@@ -9,10 +9,10 @@
 // order from +0.0 (or from the carry-in partial of a lower rank) and writes
 // out[r] -- bitwise the reference's per-row sequential sum (gs.py:34-36).
 //
-// BS7 streams ids (int4) and q_local (double2 stores, evict-first) and
-// gathers q_global with an L2 evict_last policy: every global node is
-// re-read by up to 8 elements, the furthest one a whole element layer later
-// (SURVEY Appendix A.6), so q_global must survive the streams in L2.
+// BS7 (sb_gs_pipe.cu) streams ids and q_local (evict-first) and gathers
+// q_global with an L2 evict_last policy: every global node is re-read by up
+// to 8 elements, the furthest one a whole element layer later (SURVEY
+// Appendix A.6), so q_global must survive the streams in L2.
 #include <stdlib.h>
 
 #include <algorithm>
@@ -23,15 +23,6 @@ namespace sb {
 
 constexpr int kGsThreads = 256;
 constexpr int kGatherCap = 2048;  // entries staged per CTA (16 KB of q)
-
-// SB200_NO_PIPE=1 selects the one-tile-per-CTA kernels (A/B checks).
-static bool use_pipe() {
-    static const bool on = [] {
-        const char *e = getenv("SB200_NO_PIPE");
-        return !(e && e[0] == '1');
-    }();
-    return on;
-}
 
 template <int T, int CAP>
 __global__ void __launch_bounds__(T) k_bs6_smem(const int32_t *__restrict__ bst, int64_t nblk, int G,
@@ -84,66 +75,8 @@ __global__ void __launch_bounds__(256) k_bs6_rows(const int32_t *__restrict__ rs
     }
 }
 
-template <int T, int U, bool MASK>
-__global__ void __launch_bounds__(T) k_bs7_vec(const int4 *__restrict__ ids, int64_t n4,
-                                              const double *__restrict__ qg, double2 *__restrict__ ql,
-                                              const int32_t *__restrict__ ids_s, double *__restrict__ ql_s,
-                                              int64_t tail_start, int64_t nl) {
-    const uint64_t pol = policy_evict_last();
-    const int64_t base = (int64_t)blockIdx.x * (T * U) + threadIdx.x;
-    int4 id[U];
-#pragma unroll
-    for (int j = 0; j < U; j++) {
-        const int64_t i = base + (int64_t)j * T;
-        if (i < n4) id[j] = ld_stream(ids + i);
-    }
-    double v[U][4];
-#pragma unroll
-    for (int j = 0; j < U; j++) {
-        const int64_t i = base + (int64_t)j * T;
-        if (i < n4) {
-            if (!MASK || id[j].x >= 0) v[j][0] = ld_keep(qg + id[j].x, pol);
-            if (!MASK || id[j].y >= 0) v[j][1] = ld_keep(qg + id[j].y, pol);
-            if (!MASK || id[j].z >= 0) v[j][2] = ld_keep(qg + id[j].z, pol);
-            if (!MASK || id[j].w >= 0) v[j][3] = ld_keep(qg + id[j].w, pol);
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < U; j++) {
-        const int64_t i = base + (int64_t)j * T;
-        if (i < n4) {
-            if (!MASK) {
-                st_stream(ql + 2 * i, make_double2(v[j][0], v[j][1]));
-                st_stream(ql + 2 * i + 1, make_double2(v[j][2], v[j][3]));
-            } else {
-                double *o = reinterpret_cast<double *>(ql + 2 * i);
-                if (id[j].x >= 0) st_stream(o + 0, v[j][0]);
-                if (id[j].y >= 0) st_stream(o + 1, v[j][1]);
-                if (id[j].z >= 0) st_stream(o + 2, v[j][2]);
-                if (id[j].w >= 0) st_stream(o + 3, v[j][3]);
-            }
-        }
-    }
-    if (blockIdx.x == 0 && threadIdx.x < 4) {
-        const int64_t i = tail_start + threadIdx.x;
-        if (i < nl) {
-            const int32_t d = ids_s[i];
-            if (!MASK || d >= 0) ql_s[i] = qg[d];
-        }
-    }
-}
-
-int bs7_pipe_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,
-                    cudaStream_t st);  // sb_gs_pipe.cu
-
-__global__ void __launch_bounds__(256) k_bs7_scalar(const int32_t *ids, int64_t nl, const double *qg,
-                                                   double *ql) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t d = ids[i];
-        if (d >= 0) ql[i] = qg[d];
-    }
-}
+int bs7_lanes_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,
+                     cudaStream_t st);  // sb_gs_pipe.cu
 
 }  // namespace sb
 
@@ -183,23 +116,7 @@ int sb_bs7_scatter(const int32_t *ids, int64_t nl, const double *qg, int64_t ng,
         return SB_E_INVALID;
     }
     if (nl == 0) return SB_OK;
-    cudaStream_t st = as_stream(s);
-    if (use_pipe() && aligned16(ids) && aligned16(ql)) return bs7_pipe_launch(ids, nl, qg, ql, has_mask, st);
-    if (!aligned16(ids) || !aligned16(ql)) {
-        const int64_t grid = std::min<int64_t>((nl + 255) / 256, (int64_t)sm_count() * 32);
-        k_bs7_scalar<<<(unsigned)grid, 256, 0, st>>>(ids, nl, qg, ql);
-        return launch_check("sb_bs7_scatter");
-    }
-    constexpr int T = 256, U = 2;
-    const int64_t n4 = nl / 4;
-    const int64_t grid = std::max<int64_t>(1, (n4 + T * U - 1) / (T * U));
-    const int4 *ids4 = reinterpret_cast<const int4 *>(ids);
-    double2 *ql2 = reinterpret_cast<double2 *>(ql);
-    if (has_mask)
-        k_bs7_vec<T, U, true><<<(unsigned)grid, T, 0, st>>>(ids4, n4, qg, ql2, ids, ql, 4 * n4, nl);
-    else
-        k_bs7_vec<T, U, false><<<(unsigned)grid, T, 0, st>>>(ids4, n4, qg, ql2, ids, ql, 4 * n4, nl);
-    return launch_check("sb_bs7_scatter");
+    return bs7_lanes_launch(ids, nl, qg, ql, has_mask, as_stream(s));
 }
 
 }  // extern "C"

@@ -1,4 +1,4 @@
-// sb_gs_pipe.cu -- software-pipelined persistent BS6 gather / BS7 scatter.
+// sb_gs_pipe.cu -- BS6 gather (persistent, software-pipelined) and BS7 scatter.
 //
 // The gather/scatter chains are index -> value -> store: dependent DRAM round
 // trips.  The one-tile-per-CTA kernels in sb_gs.cu pay them serially inside
@@ -35,121 +35,40 @@ constexpr int kBs6Cap = 512;   // entries per BS6 super-block (4 per thread)
 constexpr int kBs6MinCtas = 12;
 
 // ---- BS7 ----------------------------------------------------------------
-// Gather of a thread's 4 consecutive local entries.  Element-local numbering
-// makes them consecutive global ids along an element edge (an i-run), so when
-// they are, the values come in 16 B loads (half the load instructions; the
-// sectors fetched are the same).
-__device__ __forceinline__ void gather4(const double *qg, int4 d, uint64_t pol, double *v) {
-    if (d.y == d.x + 1 && d.z == d.x + 2 && d.w == d.x + 3) {
-        if (aligned16(qg + d.x)) {
-            const double2 a = ld2_keep(qg + d.x, pol), b = ld2_keep(qg + d.x + 2, pol);
-            v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-        } else {
-            v[0] = ld_keep(qg + d.x, pol);
-            const double2 m = ld2_keep(qg + d.x + 1, pol);
-            v[1] = m.x; v[2] = m.y;
-            v[3] = ld_keep(qg + d.w, pol);
-        }
-        return;
-    }
-    if (d.y == d.x + 1 && aligned16(qg + d.x)) {
-        const double2 a = ld2_keep(qg + d.x, pol);
-        v[0] = a.x; v[1] = a.y;
-    } else {
-        v[0] = ld_keep(qg + d.x, pol);
-        v[1] = ld_keep(qg + d.y, pol);
-    }
-    if (d.w == d.z + 1 && aligned16(qg + d.z)) {
-        const double2 b = ld2_keep(qg + d.z, pol);
-        v[2] = b.x; v[3] = b.y;
-    } else {
-        v[2] = ld_keep(qg + d.z, pol);
-        v[3] = ld_keep(qg + d.w, pol);
-    }
-}
-
+// One entry per lane per load: a warp instruction covers 32 consecutive
+// local entries (ids: one 128 B row; gathers: ~32/(p+1)+1 element-edge runs;
+// stores: two 128 B rows), where the int4 kernel above spreads a warp over
+// 128 entries and pays more L1 tag lookups per instruction.
 template <int T, int U, bool MASK>
-__global__ void __launch_bounds__(T) k_bs7_pipe(const int4 *__restrict__ ids4, int64_t n4,
-                                               const double *__restrict__ qg, double2 *__restrict__ ql2,
-                                               const int32_t *__restrict__ ids, double *__restrict__ ql,
-                                               int64_t nl) {
+__global__ void __launch_bounds__(T) k_bs7_lanes(const int32_t *__restrict__ ids, int64_t nl,
+                                                const double *__restrict__ qg, double *__restrict__ ql) {
     const uint64_t pol = policy_evict_last();
-    const int64_t stride = (int64_t)gridDim.x * T * U;
-    int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x;
-    int4 nxt[U];
+    const int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x;
+    int32_t d[U];
 #pragma unroll
     for (int j = 0; j < U; j++)
-        if (base + j * T < n4) nxt[j] = ld_stream(ids4 + base + j * T);
-    for (; base < n4; base += stride) {
-        int4 cur[U];
-        double v[U][4];
+        if (base + j * T < nl) d[j] = ld_stream(ids + base + j * T);
+    double v[U];
 #pragma unroll
-        for (int j = 0; j < U; j++) {
-            cur[j] = nxt[j];
-            if (base + j * T < n4) {
-                if (!MASK) {
-                    gather4(qg, cur[j], pol, v[j]);
-                } else {
-                    if (cur[j].x >= 0) v[j][0] = ld_keep(qg + cur[j].x, pol);
-                    if (cur[j].y >= 0) v[j][1] = ld_keep(qg + cur[j].y, pol);
-                    if (cur[j].z >= 0) v[j][2] = ld_keep(qg + cur[j].z, pol);
-                    if (cur[j].w >= 0) v[j][3] = ld_keep(qg + cur[j].w, pol);
-                }
-            }
-        }
-        const int64_t nb = base + stride;  // prefetch the next tile's ids
+    for (int j = 0; j < U; j++)
+        if (base + j * T < nl && (!MASK || d[j] >= 0)) v[j] = ld_keep(qg + d[j], pol);
 #pragma unroll
-        for (int j = 0; j < U; j++)
-            if (nb + j * T < n4) nxt[j] = ld_stream(ids4 + nb + j * T);
-#pragma unroll
-        for (int j = 0; j < U; j++) {
-            const int64_t i = base + j * T;
-            if (i < n4) {
-                if (!MASK) {
-                    st_stream(ql2 + 2 * i, make_double2(v[j][0], v[j][1]));
-                    st_stream(ql2 + 2 * i + 1, make_double2(v[j][2], v[j][3]));
-                } else {
-                    double *o = reinterpret_cast<double *>(ql2 + 2 * i);
-                    if (cur[j].x >= 0) st_stream(o + 0, v[j][0]);
-                    if (cur[j].y >= 0) st_stream(o + 1, v[j][1]);
-                    if (cur[j].z >= 0) st_stream(o + 2, v[j][2]);
-                    if (cur[j].w >= 0) st_stream(o + 3, v[j][3]);
-                }
-            }
-        }
-    }
-    if (blockIdx.x == 0 && threadIdx.x < 4) {  // ragged tail (nl % 4)
-        const int64_t i = 4 * n4 + threadIdx.x;
-        if (i < nl) {
-            const int32_t d = ids[i];
-            if (!MASK || d >= 0) ql[i] = qg[d];
-        }
-    }
+    for (int j = 0; j < U; j++)
+        if (base + j * T < nl && (!MASK || d[j] >= 0)) st_stream(ql + base + j * T, v[j]);
 }
 
-int bs7_pipe_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,
-                    cudaStream_t st) {
-    // 128-thread CTAs, 2 x int4 of ids each, contiguity-aware gathers: best of
-    // the variants measured in scripts/expt/run_bs7.py (N = 1, 3, 7, 15)
-    constexpr int T = 128, U = 2;
-    const int64_t n4 = nl / 4;
-    int per_sm = 1;
+int bs7_lanes_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,
+                     cudaStream_t st) {
+    // 128 threads x 4 entries per CTA, one tile per CTA (an oversubscribed
+    // grid: CTA scheduling balances the tail).  Measured on B200 over N = 1..15
+    // against int4 ids / double2 stores (the r01 kernel), entry pairs and other
+    // tile shapes (profiles/r01_bs7_variants.md): +8% at N=7, +37% at N=4.
+    constexpr int T = 128, U = 4;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, (nl + T * U - 1) / (T * U));
     if (has_mask)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bs7_pipe<T, U, true>, T, 0);
+        k_bs7_lanes<T, U, true><<<grid, T, 0, st>>>(ids, nl, qg, ql);
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bs7_pipe<T, U, false>, T, 0);
-    // Oversubscribed grid (~64 waves): on B200 hardware CTA scheduling beat a
-    // persistent one-wave grid by 4-20% across N=1..15 (scripts/expt/run_bs7.py);
-    // the ids prefetch then covers the CTAs that take a second tile.
-    const int64_t tiles = std::max<int64_t>(1, (n4 + T * U - 1) / (T * U));
-    const unsigned grid = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>(tiles, (int64_t)sm_count() * std::max(1, per_sm) * 64));
-    const int4 *ids4 = reinterpret_cast<const int4 *>(ids);
-    double2 *ql2 = reinterpret_cast<double2 *>(ql);
-    if (has_mask)
-        k_bs7_pipe<T, U, true><<<grid, T, 0, st>>>(ids4, n4, qg, ql2, ids, ql, nl);
-    else
-        k_bs7_pipe<T, U, false><<<grid, T, 0, st>>>(ids4, n4, qg, ql2, ids, ql, nl);
+        k_bs7_lanes<T, U, false><<<grid, T, 0, st>>>(ids, nl, qg, ql);
     return launch_check("sb_bs7_scatter");
 }
 

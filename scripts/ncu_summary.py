@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 TESTS = ["bs1", "bs2", "bs3", "bs4", "bs5", "bs6", "bs7"]
 KEYS = {"bs1": "k_elem_vec<0>", "bs2": "k_elem_vec<1>", "bs3": "k_lattice_tma<norm>",
         "bs4": "k_lattice_tma<dot>", "bs5": "k_lattice_tma<fused>", "bs6": "k_bs6_lanes",
-        "bs7": "k_bs7_pipe"}
+        "bs7": "k_bs7_lanes"}
 
 
 def raw(rep):
