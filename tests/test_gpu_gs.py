@@ -213,3 +213,38 @@ def test_pipelined_bs6_matches_unplanned(sb, K, p, npb):
         bs6_gather_into(op, q, a, c)
         bs6_gather_into(plain, q, b, c)
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("seed,ng,nl,hot", [(3, 7000, 30000, 300), (4, 2000, 2000, 0), (5, 50000, 180000, 490)])
+def test_planned_bs6_general_operator(sb, oracle, seed, ng, nl, hot):
+    """Pipelined BS6 on a non-mesh operator: empty rows, a row of `hot` entries
+    (up to nodes_per_block), random columns -- bitwise the oracle gather."""
+    from paper_2009_10917_b200 import _lib
+    from paper_2009_10917_b200 import mesh as M
+    from paper_2009_10917_b200.gs import bs6_gather_into
+    rng = np.random.default_rng(seed)
+    l2g = rng.integers(0, ng, nl).astype(np.int32)
+    l2g[l2g == 17] = 18          # row 17 empty
+    if hot:
+        l2g[rng.choice(nl, hot, replace=False)] = 5   # one long row
+    l2g_d = torch.from_numpy(l2g).cuda()
+    L = _lib.lib()
+    rs = torch.empty(ng + 1, dtype=torch.int32, device="cuda")
+    ci = torch.empty(nl, dtype=torch.int32, device="cuda")
+    tmp = torch.empty(int(L.sb_build_gather_general_temp_bytes(nl)), dtype=torch.uint8, device="cuda")
+    stats = torch.empty(2, dtype=torch.int64, device="cuda")
+    _lib.check(L.sb_build_gather_general(l2g_d.data_ptr(), nl, ng, rs.data_ptr(), ci.data_ptr(),
+                                         tmp.data_ptr(), tmp.shape[0], stats.data_ptr(),
+                                         _lib.stream_handle()), "general")
+    npb = 512
+    bst = M._block_starts(rs, ng, npb)
+    op = M.GatherOp(ng=ng, row_starts=rs, col_ids=ci, block_starts=bst, nodes_per_block=npb)
+    assert op.plan() is not None
+    q = rng.uniform(-1, 1, nl)
+    out = torch.empty(ng, dtype=torch.float64, device="cuda")
+    bs6_gather_into(op, d(q), out)
+    rs_o, ci_o, _ = oracle.build_gather(l2g, ng, npb)
+    want = oracle.bs6_gather(rs_o, ci_o, q)
+    got = h(out)
+    assert np.array_equal(got, want)
+    assert got[17] == 0.0 and not np.signbit(got[17])
