@@ -39,6 +39,18 @@ __global__ void __launch_bounds__(T) k_bs6_smem(const int32_t *__restrict__ bst,
     const int32_t e0 = __ldg(rs + r0);
     const int ne = __ldg(rs + r1) - e0;
     constexpr int M = CAP / T;
+    if (ne > CAP || nrows > CAP) {
+        // blocks that do not fit the tile (empty rows padding a block past CAP
+        // rows, or block_starts not packed to nodes_per_block): rows straight
+        // from global memory, same ascending order
+        for (int k = threadIdx.x; k < nrows; k += T) {
+            const int64_t r = (int64_t)r0 + k;
+            double acc = r < ncarry ? carry[r] : 0.0;
+            for (int32_t c = rs[r], e = rs[r + 1]; c < e; c++) acc = add(acc, __ldg(q + ci[c]));
+            st_stream(out + r, acc);
+        }
+        return;
+    }
     int32_t cols[M];
 #pragma unroll
     for (int m = 0; m < M; m++) {

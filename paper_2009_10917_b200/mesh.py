@@ -86,6 +86,9 @@ class ScatterIds:
         return self._minmax[1]
 
 
+BS6_PLAN_CAP = 512  # entries (and rows) per super-block, kBs6Cap in csrc/sb_gs_pipe.cu
+
+
 @dataclass(frozen=True)
 class GatherOp:
     """mesh.py:54-70: CSR of the gather operator with row blocks of bounded nonzero count."""
@@ -104,6 +107,20 @@ class GatherOp:
     def n_blocks(self) -> int:
         return int(self.block_starts.shape[0]) - 1
 
+    def _superblock_extent(self) -> tuple[int, int]:
+        """(rows, entries) of the largest super-block of the BS6 plan (G =
+        CAP // npb operator blocks each).  Both are <= CAP for operators from
+        build_gather; a hand-built one (empty rows, or blocks not packed to
+        nodes_per_block) can exceed them and then takes the unplanned path."""
+        g = max(1, BS6_PLAN_CAP // self.nodes_per_block)
+        bst = self.block_starts
+        idx = torch.arange(0, self.n_blocks + g, g, device=bst.device).clamp_(max=self.n_blocks)
+        rows = bst[idx].long()
+        if rows.numel() < 2:
+            return 0, 0
+        ents = self.row_starts[rows].long()
+        return int((rows[1:] - rows[:-1]).max().item()), int((ents[1:] - ents[:-1]).max().item())
+
     def plan(self) -> torch.Tensor | None:
         """Super-block plan for the pipelined BS6 kernel (sb_bs6_make_plan),
         built once per operator; None when the operator does not qualify."""
@@ -116,6 +133,8 @@ class GatherOp:
                 and os.environ.get("SB200_NO_PIPE") != "1"):
             L = _lib.lib()
             size = int(L.sb_bs6_plan_size(self.n_blocks, self.nodes_per_block))
+            if size > 0 and max(self._superblock_extent()) > BS6_PLAN_CAP:
+                size = 0  # a super-block would exceed the kernel's row / entry capacity
             if size > 0:
                 dev = self.row_starts.device
                 p = torch.empty(size, dtype=torch.int32, device=dev)
@@ -176,6 +195,9 @@ def _max_row_len(K: int) -> int:
 
 
 def _block_starts(row_starts: torch.Tensor, ng: int, npb: int) -> torch.Tensor:
+    """mesh.py:136-143 greedy packing on the device.  Rows must be non-empty
+    (build_gather rejects uncovered ids first, like the reference), which
+    bounds every block to <= npb rows."""
     dev = row_starts.device
     L = _lib.lib()
     st = _lib.stream_handle(dev)

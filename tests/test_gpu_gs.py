@@ -243,8 +243,36 @@ def test_planned_bs6_general_operator(sb, oracle, seed, ng, nl, hot):
     q = rng.uniform(-1, 1, nl)
     out = torch.empty(ng, dtype=torch.float64, device="cuda")
     bs6_gather_into(op, d(q), out)
-    rs_o, ci_o, _ = oracle.build_gather(l2g, ng, npb)
+    counts = np.bincount(l2g, minlength=ng)        # mesh.py:123-134 without the coverage check
+    rs_o = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    ci_o = np.argsort(l2g, kind="stable").astype(np.int32)
+    assert np.array_equal(h(rs), rs_o) and np.array_equal(h(ci), ci_o)
     want = oracle.bs6_gather(rs_o, ci_o, q)
     got = h(out)
     assert np.array_equal(got, want)
     assert got[17] == 0.0 and not np.signbit(got[17])
+
+
+def test_planned_bs6_many_empty_rows_falls_back(sb, oracle):
+    """A hand-built operator whose blocks hold > 512 (empty) rows must not use
+    the super-block kernel's fixed row capacity -- result still bitwise."""
+    from paper_2009_10917_b200 import mesh as M
+    from paper_2009_10917_b200.gs import bs6_gather_into
+    ng, nl = 5000, 3000
+    rng = np.random.default_rng(9)
+    l2g = np.sort(rng.choice(ng, nl, replace=False)).astype(np.int32)   # 2000 empty rows
+    counts = np.bincount(l2g, minlength=ng)
+    rs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    ci = np.argsort(l2g, kind="stable").astype(np.int32)
+    bst, row = [0], 0
+    while row < ng:  # mesh.py:136-143, the reference's greedy packing (empty rows included)
+        nxt = min(max(int(np.searchsorted(rs, int(rs[row]) + 512, side="right")) - 1, row + 1), ng)
+        bst.append(nxt)
+        row = nxt
+    op = M.GatherOp(ng=ng, row_starts=torch.from_numpy(rs).cuda(), col_ids=torch.from_numpy(ci).cuda(),
+                    block_starts=torch.tensor(bst, dtype=torch.int32, device="cuda"), nodes_per_block=512)
+    assert op._superblock_extent()[0] > 512 and op.plan() is None
+    q = rng.uniform(-1, 1, nl)
+    out = torch.empty(ng, dtype=torch.float64, device="cuda")
+    bs6_gather_into(op, d(q), out)
+    assert np.array_equal(h(out), oracle.bs6_gather(rs, ci, q))
