@@ -21,6 +21,7 @@
 // Results are bitwise those of the one-tile kernels: BS6 still sums each row
 // in ascending column order from +0.0 (or the carry-in) in one thread.
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -218,8 +219,8 @@ __device__ __forceinline__ void bs6_publish_vals(const SbMeta &m, const double2 
 // and (2t+2T, 2t+2T+1) of its super-block, gathered with one 16 B load when
 // the two columns are adjacent (the 8-entry rows of p = 1 meshes pair up
 // often enough for that to beat one entry per lane).
-template <int T, int CAP, bool SWZ>
-__global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pairs(const int32_t *__restrict__ plan, int64_t nsb,
+template <int T, int CAP, bool SWZ, int MINB = kBs6MinCtas>
+__global__ void __launch_bounds__(T, MINB) k_bs6_pairs(const int32_t *__restrict__ plan, int64_t nsb,
                                                              const int32_t *__restrict__ rs,
                                                              const int32_t *__restrict__ ci,
                                                              const double *__restrict__ q,
@@ -258,8 +259,8 @@ __global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_pairs(const int32_t *__r
 // (4 element-edge runs of 8 at N=7 -> ~4 lines) whatever the parity of the
 // run starts, and the column loads are fully coalesced 128 B rows; paired
 // 16 B gathers only pay off when a run starts on an even entry.
-template <int T, int CAP, bool SWZ>
-__global__ void __launch_bounds__(T, kBs6MinCtas) k_bs6_lanes(const int32_t *__restrict__ plan, int64_t nsb,
+template <int T, int CAP, bool SWZ, int MINB = kBs6MinCtas>
+__global__ void __launch_bounds__(T, MINB) k_bs6_lanes(const int32_t *__restrict__ plan, int64_t nsb,
                                                              const int32_t *__restrict__ rs,
                                                              const int32_t *__restrict__ ci,
                                                              const double *__restrict__ q,
@@ -353,30 +354,34 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     const size_t smem = 2 * kBs6Cap * sizeof(double);
     using KernT = void (*)(const int32_t *, int64_t, const int32_t *, const int32_t *, const double *, double *,
                            const double *, int64_t);
-    static thread_local int attr_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (attr_dev != dev) {
-        const KernT all[4] = {k_bs6_pairs<T, kBs6Cap, true>, k_bs6_pairs<T, kBs6Cap, false>,
-                              k_bs6_lanes<T, kBs6Cap, true>, k_bs6_lanes<T, kBs6Cap, false>};
-        for (KernT k : all)
-            if (cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                           "sb_bs6_gather_planned: shared memory attribute"))
-                return SB_E_CUDA;
-        attr_dev = dev;
+    // Kernel, value-tile swizzle and CTAs per SM by the mean row length
+    // rho = nl/ng (measured on B200 over N = 1..15, profiles/r01_bs6_variants.md):
+    //   rho >= 4    (p = 1)   pairs, swizzled, 12 CTAs/SM (40 registers)
+    //   rho >= 3    (p = 2)   lanes, plain,    12 CTAs/SM
+    //   rho >= 2.2  (p = 3)   lanes, swizzled,  8 CTAs/SM (64 registers)
+    //   rho <  2.2  (p >= 4)  lanes, plain,    10 CTAs/SM (48 registers)
+    // SB200_BS6_CFG="<lanes|pairs>,<swizzle 0|1>,<CTAs/SM 6|8|10|12>" overrides
+    // the choice (A/B runs, scripts/expt/time_bs6.py).
+    bool pairs, sw;
+    int mb;
+    if (nl >= 4 * ng) { pairs = true; sw = true; mb = 12; }
+    else if (nl >= 3 * ng) { pairs = false; sw = false; mb = 12; }
+    else if (5 * nl >= 11 * ng) { pairs = false; sw = true; mb = 8; }
+    else { pairs = false; sw = false; mb = 10; }
+    static const char *cfg = getenv("SB200_BS6_CFG");
+    if (cfg) {
+        pairs = cfg[0] == 'p';
+        const char *c1 = strchr(cfg, ',');
+        sw = c1 && c1[1] == '1';
+        const char *c2 = c1 ? strchr(c1 + 1, ',') : nullptr;
+        mb = c2 ? atoi(c2 + 1) : 12;
     }
-    // Kernel and value-tile swizzle by mean row length nl/ng (measured on B200
-    // over N = 1..15, scripts/expt/time_bs6.py): pairs + swizzle for the long
-    // rows of p = 1; one entry per lane otherwise, swizzled for rho <= 1.6
-    // (p >= 7), where the row-sum reads otherwise hit 3x the ideal wavefronts.
-    KernT kern;
-    if (nl >= 4 * ng)
-        kern = k_bs6_pairs<T, kBs6Cap, true>;
-    else if (5 * nl > 8 * ng)
-        kern = k_bs6_lanes<T, kBs6Cap, false>;
-    else
-        kern = k_bs6_lanes<T, kBs6Cap, true>;
-    int per_sm = 1;
+#define SB_PICK(K_, MB_) (sw ? K_<T, kBs6Cap, true, MB_> : K_<T, kBs6Cap, false, MB_>)
+#define SB_PICK_MB(K_) (mb == 6 ? SB_PICK(K_, 6) : mb == 8 ? SB_PICK(K_, 8) : mb == 10 ? SB_PICK(K_, 10) : SB_PICK(K_, 12))
+    const KernT kern = pairs ? SB_PICK_MB(k_bs6_pairs) : SB_PICK_MB(k_bs6_lanes);
+#undef SB_PICK_MB
+#undef SB_PICK
+    int per_sm = 1;  // (8 KB of dynamic shared memory: below the default limit)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
     const int64_t grid = std::min<int64_t>(nsb, (int64_t)sm_count() * std::max(1, per_sm));
     kern<<<(unsigned)std::max<int64_t>(1, grid), T, smem, as_stream(s)>>>(plan, nsb, rs, ci, q, out, carry,

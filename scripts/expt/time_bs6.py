@@ -9,7 +9,7 @@ sys.path.insert(0, ROOT)
 import paper_2009_10917_b200 as sb  # noqa: E402
 from paper_2009_10917_b200.core import bytes_moved  # noqa: E402
 
-tag = "k" + os.environ.get("SB200_BS6_KERNEL", "3")
+tag = os.environ.get("SB200_BS6_CFG", "default")
 orders = [int(a) for a in sys.argv[1:]] or [1, 2, 3, 5, 7, 10, 15]
 for p in orders:
     K = int(round((1e8 ** (1 / 3) - 1) / p))
