@@ -530,6 +530,7 @@ def main_ours(args):
                        "n_per_gpu": int(args.n), "mesh": w.mesh_desc,
                        "reduction": [args.block_size, args.n_blocks],
                        "parallelism": f"slab{world}" if world > 1 else "single",
+                       **({"collective": dist_ctx.collective} if dist_ctx is not None else {}),
                        "l2": "every input > L2 (126 MB); no flush between steps"},
             "frac_of_peak": round(value / agg_peak, 4),
             "per_test": per_test, "roofline": roof,

@@ -230,6 +230,30 @@ int sb_cg_update(int fused, const double *p, const double *ap, double *x, double
 int sb_cg_direction(const double *r, double *p, int64_t n, sb_cg_state *state,
                     sb_stream_t stream);
 
+
+/* ---- fused multi-GPU reductions -----------------------
+ * BS3/BS4/BS5 whose last CTA also combines the per-rank scalars over NVLink
+ * peer memory (NCCL 2.28 device API, LSA windows): the rank's value is
+ * stored into every peer's symmetric window, the ranks meet at an LSA
+ * barrier, and each sums the values in rank order from +0.0 -- bitwise the
+ * all-gather + sb_sum_ordered result, in a single launch.  Collective: every
+ * rank of the context must make the same sequence of calls, one stream per
+ * context.  Needs libnccl.so.2 >= 2.28 in the process (torch's) and every
+ * rank NVLink-reachable; otherwise sb_lsa_create returns SB_E_INVALID. */
+typedef struct sb_lsa sb_lsa_t;
+int sb_lsa_unique_id(void *out, size_t bytes);  /* rank 0; bytes >= 128 */
+int sb_lsa_create(const void *unique_id, size_t bytes, int nranks, int rank, sb_lsa_t **out);
+int sb_lsa_destroy(sb_lsa_t *ctx);
+int sb_lsa_bs3_norm2(const double *x, int64_t n, int64_t block_size, int64_t n_blocks,
+                     void *workspace, double *result, sb_lsa_t *ctx, sb_stream_t stream);
+int sb_lsa_bs4_dot(const double *x, const double *y, int64_t n, int64_t block_size,
+                   int64_t n_blocks, void *workspace, double *result, sb_lsa_t *ctx,
+                   sb_stream_t stream);
+int sb_lsa_bs5_fused_cg_update(double alpha, const double *p, const double *ap, double *x,
+                               double *r, int64_t n, int64_t block_size, int64_t n_blocks,
+                               void *workspace, double *result, sb_lsa_t *ctx,
+                               sb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,13 @@ _SIGS = {
     "sb_cg_update": (_c_int, [_c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp,
                               _c_vp]),
     "sb_cg_direction": (_c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_vp]),
+    "sb_lsa_unique_id": (_c_int, [_c_vp, _c_size]),
+    "sb_lsa_create": (_c_int, [_c_vp, _c_size, _c_int, _c_int, _c_vp]),
+    "sb_lsa_destroy": (_c_int, [_c_vp]),
+    "sb_lsa_bs3_norm2": (_c_int, [_c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "sb_lsa_bs4_dot": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "sb_lsa_bs5_fused_cg_update": (_c_int, [_c_dbl, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64,
+                                            _c_vp, _c_vp, _c_vp, _c_vp]),
     "sb_bs6_make_plan": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_vp]),
     "sb_bs6_gather_planned": (_c_int, [_c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp,
                                        _c_vp, _c_vp, _c_i64, _c_vp]),

@@ -28,6 +28,19 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-
          "--expt-relaxed-constexpr"]
 
 
+def nccl_include() -> str:
+    """NCCL >= 2.28 headers (nccl_device.h) from the nvidia-nccl wheel torch uses;
+    /usr/include/nccl.h is an older release without the device API."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    roots = list(spec.submodule_search_locations) if spec and spec.submodule_search_locations else []
+    for r in roots:
+        inc = os.path.join(r, "include")
+        if os.path.exists(os.path.join(inc, "nccl_device.h")):
+            return inc
+    raise RuntimeError("nccl_device.h (NCCL >= 2.28 headers) not found in the nvidia-nccl package")
+
+
 def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -49,13 +62,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, "-I" + nccl_include(), "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"], check=True)
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-ldl"], check=True)
     os.replace(tmp, LIB)
     return LIB
 

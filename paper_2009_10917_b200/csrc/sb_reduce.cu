@@ -24,6 +24,7 @@
 #include <algorithm>
 
 #include "sb_common.cuh"
+#include "sb_lsa.cuh"
 
 namespace sb {
 
@@ -59,7 +60,18 @@ struct RArgs {
     // device CG: *gate == 0 -> every CTA returns; alpha read from *alpha_ptr
     const int32_t *gate;
     const double *alpha_ptr;
+    // multi-GPU fused combine (sb_lsa.cuh): the last CTA publishes the rank's
+    // scalar to every NVLink peer and sums the ranks' scalars in rank order
+    LsaArgs lsa;
 };
+
+// Thread 0 of the last CTA: write the block-reduced scalar.
+__device__ __forceinline__ void write_result(const RArgs &A, double v) {
+    if (A.lsa.enabled)
+        *A.result = lsa_combine(A.lsa, v);
+    else
+        *A.result = v;
+}
 
 // Gate check + device alpha at kernel entry (a no-op for plain calls).
 __device__ __forceinline__ bool resolve(RArgs &A) {
@@ -161,7 +173,7 @@ __device__ __forceinline__ void second_stage(const RArgs &A, double *sm, int bs,
     __syncthreads();
     const double res = tree_fold<T>(sm, bs);
     if (threadIdx.x == 0) {
-        *A.result = res;
+        write_result(A, res);
         *A.ticket = 0u;  // workspace left ready for the next call on this stream
     }
 }
@@ -376,7 +388,7 @@ __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs Ain) {
         double r = tid < W ? sm[tid] : 0.0;
         for (int off = W / 2; off >= 1; off >>= 1) r = add(r, __shfl_down_sync(0xffffffffu, r, off));
         if (tid == 0) {
-            *A.result = r;
+            write_result(A, r);
             *A.ticket = 0u;
         }
     }
@@ -424,7 +436,7 @@ __global__ void __launch_bounds__(1024) k_final_generic(RArgs A) {
     }
     __syncthreads();
     const double v = fold_global_row(srow, A.bs);
-    if (threadIdx.x == 0) *A.result = v;
+    if (threadIdx.x == 0) write_result(A, v);
 }
 
 // block_size 512 halves the steps per stage (same stage bytes)
@@ -531,6 +543,23 @@ int cg_reduce(int mode, const double *u, const double *v, double *x, double *r, 
     A.u = u; A.v = v; A.x = x; A.r = r; A.n = n; A.bs = bs; A.nb = nb; A.result = result;
     A.gate = gate; A.alpha_ptr = alpha;
     if (!gate || (n > 0 && (!u || !v || (mode == R_FUSED && (!x || !r || !alpha))))) {
+        set_error("%s: invalid arguments", name);
+        return SB_E_INVALID;
+    }
+    switch (mode) {
+        case R_NORM: return launch_reduce<R_NORM>(A, ws, st, name);
+        case R_DOT: return launch_reduce<R_DOT>(A, ws, st, name);
+        default: return launch_reduce<R_FUSED>(A, ws, st, name);
+    }
+}
+
+int lsa_reduce(int mode, double alpha, const double *u, const double *v, double *x, double *r, int64_t n,
+               int64_t bs, int64_t nb, void *ws, double *result, const LsaArgs &lsa, cudaStream_t st,
+               const char *name) {
+    RArgs A{};
+    A.u = u; A.v = v; A.x = x; A.r = r; A.alpha = alpha; A.n = n; A.bs = bs; A.nb = nb; A.result = result;
+    A.lsa = lsa;
+    if (n > 0 && (!u || !v || (mode == R_FUSED && (!x || !r)))) {
         set_error("%s: invalid arguments", name);
         return SB_E_INVALID;
     }

@@ -284,9 +284,23 @@ class _Ids:
 class BenchContext:
     """Per-rank state of bench.py's weak-scaling step (n per rank, K_g^3 mesh)."""
 
-    def __init__(self, rank: int, world: int, args, device):
+    def __init__(self, rank: int, world: int, args, device, use_lsa: bool | None = None):
+        import os
         self.rank, self.world, self.device = rank, world, torch.device(device)
         self.reducer = DistReducer(world, device)
+        # BS3/BS4/BS5: the reduction and the cross-rank combine fused in one
+        # kernel over NVLink peer memory (lsa.py) when every rank is an LSA
+        # peer; otherwise (or SB200_LSA=0) NCCL all-gather + ordered sum.
+        self.lsa, self.collective = None, "nccl all_gather + sb_sum_ordered"
+        if use_lsa is None:
+            use_lsa = _nccl(None) and os.environ.get("SB200_LSA", "1") != "0"
+        if use_lsa:
+            from .lsa import LsaReducer, LsaUnavailable
+            try:
+                self.lsa = LsaReducer(world, rank, device)
+                self.collective = "fused in-kernel combine over NVLink (NCCL device API, LSA window)"
+            except LsaUnavailable as e:
+                self.collective += f" (fused path unavailable: {e})"
         Kg = max(world, int(round(args.K * world ** (1.0 / 3.0))))
         self.part = SlabPartition(Kg, args.order, world)
         g = self.part.g
@@ -294,9 +308,9 @@ class BenchContext:
                           "nl_global": Kg ** 3 * (args.order + 1) ** 3,
                           "slab_layers": [self.part.layers(r) for r in range(world)],
                           "partition": "z-slabs, carry halo (BS6), one-plane halo (BS7)"}
-        # per step: 7 kernels + (3 reductions x (NCCL all-gather + ordered sum)) + BS6 send-plane
-        # gather + NCCL carry + BS7 NCCL halo
-        self.launches_per_step = 7 + 3 * 1 + 1
+        # per step: 7 kernels + BS6 send-plane gather (+ 3 ordered-sum kernels after the
+        # NCCL all-gathers when the fused combine is not in use); NCCL p2p halos not counted
+        self.launches_per_step = 7 + 1 + (0 if self.lsa is not None else 3)
 
     def build_slab(self, K, order, device):
         self.gather = DistGather.build(self.part, self.rank, device)
@@ -310,12 +324,21 @@ class BenchContext:
         elif test == "bs2":
             w.sb.bs2_axpy(0.5, w.x, -0.25, w.y)
         elif test == "bs3":
-            self.reducer.combine(KN.bs3_norm2_async(w.x, w.cfg, out=w.res), out=w.res)
+            if self.lsa is not None:
+                self.lsa.bs3_norm2(w.x, w.cfg, out=w.res)
+            else:
+                self.reducer.combine(KN.bs3_norm2_async(w.x, w.cfg, out=w.res), out=w.res)
         elif test == "bs4":
-            self.reducer.combine(KN.bs4_dot_async(w.x, w.y, w.cfg, out=w.res), out=w.res)
+            if self.lsa is not None:
+                self.lsa.bs4_dot(w.x, w.y, w.cfg, out=w.res)
+            else:
+                self.reducer.combine(KN.bs4_dot_async(w.x, w.y, w.cfg, out=w.res), out=w.res)
         elif test == "bs5":
-            self.reducer.combine(KN.bs5_fused_cg_update_async(1e-3, w.p, w.ap, w.x, w.r, w.cfg,
-                                                              out=w.res), out=w.res)
+            if self.lsa is not None:
+                self.lsa.bs5_fused_cg_update(1e-3, w.p, w.ap, w.x, w.r, w.cfg, out=w.res)
+            else:
+                self.reducer.combine(KN.bs5_fused_cg_update_async(1e-3, w.p, w.ap, w.x, w.r, w.cfg,
+                                                                  out=w.res), out=w.res)
         elif test == "bs6":
             self.gather.gather(w.q, w.gout)
         else:

@@ -1,0 +1,116 @@
+"""Fused multi-GPU BS3/BS4/BS5: the lattice reduction and
+the cross-rank combine in ONE kernel over NVLink peer memory.
+
+`LsaReducer` wraps an `sb_lsa_t` context (csrc/sb_lsa.cu): an NCCL 2.28
+communicator of its own, a symmetric window of 2 x 128 doubles and a device
+communicator with one LSA barrier.  Each call's last CTA stores the rank's
+scalar into every peer's window, meets the peers at the barrier and sums
+the ranks' values in rank order from +0.0 -- bitwise what dist.DistReducer's
+NCCL all-gather + sb_sum_ordered produces, without the separate collective.
+
+Collective semantics: every rank makes the same calls in the same order on
+one stream.  Creation needs every rank NVLink-reachable (one node); callers
+fall back to DistReducer otherwise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .kernels import DEFAULT_REDUCTION, ReductionConfig
+
+UID_BYTES = 128
+
+
+class LsaUnavailable(RuntimeError):
+    """The fused path cannot be set up here (NCCL < 2.28, ranks not NVLink peers, ...)."""
+
+
+class LsaReducer:
+    def __init__(self, world: int, rank: int, device, group=None, unique_id: bytes | None = None):
+        self.L = _lib.lib()
+        self.world, self.rank = world, rank
+        self.device = torch.device(device)
+        if unique_id is None:
+            unique_id = self._exchange_uid(group)
+        buf = ctypes.create_string_buffer(bytes(unique_id), UID_BYTES)
+        h = ctypes.c_void_p()
+        rc = self.L.sb_lsa_create(buf, UID_BYTES, world, rank, ctypes.byref(h))
+        if rc != _lib.SB_OK:
+            raise LsaUnavailable(_lib.last_error())
+        self.handle = h
+        self._ws = {}
+
+    def _exchange_uid(self, group) -> bytes:
+        t = torch.zeros(UID_BYTES, dtype=torch.uint8)
+        if self.rank == 0:
+            raw = ctypes.create_string_buffer(UID_BYTES)
+            _lib.check(self.L.sb_lsa_unique_id(raw, UID_BYTES), "sb_lsa_unique_id")
+            t = torch.frombuffer(bytearray(raw.raw), dtype=torch.uint8).clone()
+        if self.world > 1:
+            if dist.get_backend(group) == "nccl":
+                td = t.to(self.device)
+                dist.broadcast(td, 0, group=group)
+                t = td.cpu()
+            else:
+                dist.broadcast(t, 0, group=group)
+        return bytes(t.numpy().tobytes())
+
+    @staticmethod
+    def unique_id() -> bytes:
+        raw = ctypes.create_string_buffer(UID_BYTES)
+        _lib.check(_lib.lib().sb_lsa_unique_id(raw, UID_BYTES), "sb_lsa_unique_id")
+        return raw.raw
+
+    def close(self) -> None:
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self.L.sb_lsa_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # a private zeroed workspace per config (the kernels leave it zeroed)
+    def _workspace(self, cfg: ReductionConfig) -> torch.Tensor:
+        key = (cfg.block_size, cfg.n_blocks)
+        ws = self._ws.get(key)
+        if ws is None:
+            nbytes = int(self.L.sb_reduce_workspace_bytes(*key))
+            ws = self._ws[key] = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+        return ws
+
+    def _out(self, out):
+        return out if out is not None else torch.empty(1, dtype=torch.float64, device=self.device)
+
+    def bs3_norm2(self, x: torch.Tensor, cfg: ReductionConfig = DEFAULT_REDUCTION, out=None) -> torch.Tensor:
+        """kernels.py:106-108 over the ranks' chunks, combined in the same launch."""
+        res = self._out(out)
+        _lib.check(self.L.sb_lsa_bs3_norm2(x.data_ptr(), x.shape[0], cfg.block_size, cfg.n_blocks,
+                                           self._workspace(cfg).data_ptr(), res.data_ptr(), self.handle,
+                                           _lib.stream_handle(self.device)), "lsa bs3_norm2")
+        return res
+
+    def bs4_dot(self, x: torch.Tensor, y: torch.Tensor, cfg: ReductionConfig = DEFAULT_REDUCTION,
+                out=None) -> torch.Tensor:
+        res = self._out(out)
+        _lib.check(self.L.sb_lsa_bs4_dot(x.data_ptr(), y.data_ptr(), x.shape[0], cfg.block_size, cfg.n_blocks,
+                                         self._workspace(cfg).data_ptr(), res.data_ptr(), self.handle,
+                                         _lib.stream_handle(self.device)), "lsa bs4_dot")
+        return res
+
+    def bs5_fused_cg_update(self, alpha: float, p, ap, x, r, cfg: ReductionConfig = DEFAULT_REDUCTION,
+                            out=None) -> torch.Tensor:
+        res = self._out(out)
+        _lib.check(self.L.sb_lsa_bs5_fused_cg_update(float(alpha), p.data_ptr(), ap.data_ptr(), x.data_ptr(),
+                                                     r.data_ptr(), x.shape[0], cfg.block_size, cfg.n_blocks,
+                                                     self._workspace(cfg).data_ptr(), res.data_ptr(),
+                                                     self.handle, _lib.stream_handle(self.device)),
+                   "lsa bs5_fused_cg_update")
+        return res

@@ -83,3 +83,38 @@ def test_nccl_one_rank_group(sb):
         assert torch.equal(ql, sc.window[mesh.local_to_global.long()])
     finally:
         dist.destroy_process_group()
+
+
+def test_bench_context_fused_combine_one_rank(sb):
+    """BenchContext on a 1-rank NCCL group picks the fused in-kernel combine
+    (lsa.py) and its BS3/BS4/BS5 results equal the all-gather path's."""
+    import types
+    import torch.distributed as dist
+    from paper_2009_10917_b200 import dist as D
+    from paper_2009_10917_b200 import kernels as KN
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        args = types.SimpleNamespace(K=6, order=3)
+        ctx = D.BenchContext(0, 1, args, dev)
+        assert ctx.lsa is not None, ctx.collective
+        cfg = KN.ReductionConfig()
+        x, y, p, ap, r = (torch.empty(2_000_003, dtype=torch.float64, device=dev).uniform_(-1, 1)
+                          for _ in range(5))
+        w = types.SimpleNamespace(x=x, y=y, p=p, ap=ap, r=r, cfg=cfg,
+                                  res=torch.empty(1, dtype=torch.float64, device=dev), sb=sb)
+        ctx.call(w, "bs3")
+        assert w.res.item() == KN.bs3_norm2_async(x, cfg).item()
+        ctx.call(w, "bs4")
+        assert w.res.item() == 0.0 + KN.bs4_dot_async(x, y, cfg).item()
+        x0, r0 = x.clone(), r.clone()
+        ctx.call(w, "bs5")
+        got = w.res.item()
+        want = KN.bs5_fused_cg_update_async(1e-3, p, ap, x0, r0, cfg).item()
+        assert got == want and torch.equal(x, x0) and torch.equal(r, r0)
+        ctx.lsa.close()
+    finally:
+        dist.destroy_process_group()

@@ -1,0 +1,63 @@
+"""Fused BS3/BS4/BS5 + cross-rank combine over NVLink peer memory (lsa.py,
+csrc/sb_lsa.cu).  One GPU per gpurun call, so this runs the one-rank team:
+the kernel still stores into the (own) symmetric window through the LSA
+mapping, passes the LSA barrier and sums the slots -- the result must equal
+dist.DistReducer's rank-order sum (0.0 + v) bit for bit.  The multi-rank
+ordering/epoch logic is covered by test_dist_gloo.py's reference semantics."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lsa():
+    from paper_2009_10917_b200 import lsa as LSA
+    try:
+        r = LSA.LsaReducer(1, 0, "cuda:0", unique_id=LSA.LsaReducer.unique_id())
+    except LSA.LsaUnavailable as e:  # pragma: no cover - depends on the box's NCCL
+        pytest.fail(f"fused path unavailable: {e}")
+    yield r
+    r.close()
+
+
+def _v(n, seed):
+    return torch.from_numpy(np.random.default_rng(seed).uniform(-1, 1, n)).cuda()
+
+
+@pytest.mark.parametrize("n", [0, 1, 4097, 1_000_003, 20_000_000])
+def test_lsa_reductions_equal_plain(lsa, n):
+    from paper_2009_10917_b200 import kernels as KN
+    from paper_2009_10917_b200.kernels import ReductionConfig
+    for cfg in (ReductionConfig(), ReductionConfig(64, 7), ReductionConfig(1024, 1184), ReductionConfig(2048, 3)):
+        x, y, p, ap = (_v(n, s) for s in range(4))
+        want3 = KN.bs3_norm2_async(x, cfg).item()
+        want4 = KN.bs4_dot_async(x, y, cfg).item()
+        assert lsa.bs3_norm2(x, cfg).item() == 0.0 + want3
+        got4 = lsa.bs4_dot(x, y, cfg).item()
+        assert got4 == 0.0 + want4 and np.signbit(got4) == np.signbit(0.0 + want4)
+        x2, y2 = x.clone(), y.clone()
+        want5 = KN.bs5_fused_cg_update_async(0.375, p, ap, x, y, cfg).item()
+        got5 = lsa.bs5_fused_cg_update(0.375, p, ap, x2, y2, cfg).item()
+        assert got5 == 0.0 + want5
+        assert torch.equal(x2, x) and torch.equal(y2, y)
+
+
+def test_lsa_many_calls_alternate_epochs(lsa):
+    from paper_2009_10917_b200 import kernels as KN
+    x = _v(300_001, 9)
+    want = KN.bs3_norm2_async(x).item()
+    outs = [lsa.bs3_norm2(x) for _ in range(9)]
+    torch.cuda.synchronize()
+    assert all(o.item() == want for o in outs)
+
+
+def test_lsa_inside_cuda_graph_not_required_but_stream_ordered(lsa):
+    """Back-to-back fused calls on one stream with no host sync in between."""
+    from paper_2009_10917_b200 import kernels as KN
+    xs = [_v(100_000 + i, 20 + i) for i in range(6)]
+    res = [lsa.bs3_norm2(x) for x in xs]
+    want = [KN.bs3_norm2_async(x).item() for x in xs]
+    assert [r.item() for r in res] == want
