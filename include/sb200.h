@@ -244,6 +244,15 @@ typedef struct sb_lsa sb_lsa_t;
 int sb_lsa_unique_id(void *out, size_t bytes);  /* rank 0; bytes >= 128 */
 int sb_lsa_create(const void *unique_id, size_t bytes, int nranks, int rank, sb_lsa_t **out);
 int sb_lsa_destroy(sb_lsa_t *ctx);
+/* BS6 carry halo over NVLink (dist.py DistGather): a symmetric window per
+ * context (collective); sb_lsa_halo_pointers returns this rank's local
+ * address of `offset` and peer `peer`'s NVLink-mapped address of it, so the
+ * send-plane gather (sb_bs6_gather_planned) writes its partials straight
+ * into rank+1's carry buffer; sb_lsa_barrier (collective, one thread)
+ * orders those stores before rank+1's own gather reads them. */
+int sb_lsa_halo_window(sb_lsa_t *ctx, size_t bytes);
+int sb_lsa_halo_pointers(sb_lsa_t *ctx, size_t offset, int peer, void **local, void **remote);
+int sb_lsa_barrier(sb_lsa_t *ctx, sb_stream_t stream);
 int sb_lsa_bs3_norm2(const double *x, int64_t n, int64_t block_size, int64_t n_blocks,
                      void *workspace, double *result, sb_lsa_t *ctx, sb_stream_t stream);
 int sb_lsa_bs4_dot(const double *x, const double *y, int64_t n, int64_t block_size,

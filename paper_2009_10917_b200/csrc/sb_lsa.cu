@@ -67,7 +67,22 @@ struct sb_lsa {
     bool has_win = false, has_dc = false;
     int nranks = 0, rank = 0;
     long long calls = 0;
+    // BS6 carry halo window (sb_lsa_halo_window): 2 x plane doubles
+    void *hbuf = nullptr;
+    ncclWindow_t hwin{};
+    bool has_hwin = false;
+    size_t hbytes = 0;
 };
+
+namespace sb {
+__global__ void k_lsa_peer_ptr(ncclWindow_t w, size_t off, int peer, void **out) {
+    *out = ncclGetLsaPointer(w, off, peer);
+}
+__global__ void k_lsa_barrier(ncclDevComm dc) {
+    ncclLsaBarrierSession<ncclCoopThread> bar(ncclCoopThread(), dc, ncclTeamTagLsa(), 0);
+    bar.sync(ncclCoopThread(), cuda::memory_order_acq_rel);
+}
+}  // namespace sb
 
 using namespace sb;
 
@@ -91,6 +106,8 @@ static int need_api(const char *what) {
 
 static void lsa_free(sb_lsa_t *c) {
     NcclApi &a = nccl_api();
+    if (c->has_hwin) a.CommWindowDeregister(c->comm, c->hwin);
+    if (c->hbuf) a.MemFree(c->hbuf);
     if (c->has_dc) a.DevCommDestroy(c->comm, &c->dc);
     if (c->has_win) a.CommWindowDeregister(c->comm, c->win);
     if (c->buf) a.MemFree(c->buf);
@@ -176,6 +193,54 @@ static LsaArgs lsa_args(sb_lsa_t *c) {
     L.epoch = (int)(c->calls++ & 1);
     L.enabled = 1;
     return L;
+}
+
+int sb_lsa_halo_window(sb_lsa_t *ctx, size_t bytes) {
+    clear_error();
+    if (!ctx || bytes == 0 || ctx->has_hwin) {
+        set_error("sb_lsa_halo_window: invalid arguments (one halo window per context)");
+        return SB_E_INVALID;
+    }
+    NcclApi &a = nccl_api();
+    int rc = nccl_check(a.MemAlloc(&ctx->hbuf, bytes), "ncclMemAlloc");
+    if (!rc) rc = cuda_check(cudaMemset(ctx->hbuf, 0, bytes), "sb_lsa_halo_window memset");
+    if (!rc) {
+        rc = nccl_check(a.CommWindowRegister(ctx->comm, ctx->hbuf, bytes, &ctx->hwin, NCCL_WIN_COLL_SYMMETRIC),
+                        "ncclCommWindowRegister");
+        ctx->has_hwin = rc == SB_OK;
+    }
+    if (!rc) rc = cuda_check(cudaDeviceSynchronize(), "sb_lsa_halo_window");
+    if (!rc) ctx->hbytes = bytes;
+    return rc;
+}
+
+int sb_lsa_halo_pointers(sb_lsa_t *ctx, size_t offset, int peer, void **local, void **remote) {
+    clear_error();
+    if (!ctx || !ctx->has_hwin || offset >= ctx->hbytes || peer < 0 || peer >= ctx->nranks) {
+        set_error("sb_lsa_halo_pointers: invalid arguments");
+        return SB_E_INVALID;
+    }
+    if (local) *local = static_cast<char *>(ctx->hbuf) + offset;
+    if (remote) {
+        void **d = nullptr;
+        int rc = cuda_check(cudaMalloc(&d, sizeof(void *)), "sb_lsa_halo_pointers");
+        if (rc) return rc;
+        k_lsa_peer_ptr<<<1, 1>>>(ctx->hwin, offset, peer, d);
+        rc = cuda_check(cudaMemcpy(remote, d, sizeof(void *), cudaMemcpyDeviceToHost), "sb_lsa_halo_pointers");
+        cudaFree(d);
+        if (rc) return rc;
+    }
+    return SB_OK;
+}
+
+int sb_lsa_barrier(sb_lsa_t *ctx, sb_stream_t s) {
+    clear_error();
+    if (!ctx) {
+        set_error("sb_lsa_barrier: null context");
+        return SB_E_INVALID;
+    }
+    k_lsa_barrier<<<1, 1, 0, as_stream(s)>>>(ctx->dc);
+    return launch_check("sb_lsa_barrier");
 }
 
 int sb_lsa_bs3_norm2(const double *x, int64_t n, int64_t bs, int64_t nb, void *ws, double *result, sb_lsa_t *ctx,

@@ -208,6 +208,28 @@ class DistGather:
                                                          nodes_per_block, device)
         return cls(part, rank, own, send, device, group=group)
 
+    def enable_lsa(self, lsa) -> None:
+        """Collective: carry halo over NVLink peer memory (lsa.LsaReducer).
+        The send-plane gather then writes its partials straight into rank+1's
+        carry buffer (two buffers, alternating per call) and one LSA barrier
+        replaces the NCCL send/recv pair."""
+        nb = 8 * self.part.plane
+        lsa.halo_window(2 * nb)
+        self.lsa, self.epoch = lsa, 0
+        self.carry_ptrs = [lsa.halo_pointers(e * nb, self.rank)[0] for e in (0, 1)]
+        self.send_ptrs = ([lsa.halo_pointers(e * nb, self.rank + 1)[1] for e in (0, 1)]
+                          if self.send_op is not None else None)
+
+    def gather_lsa(self, q_slab: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        e = self.epoch
+        self.epoch ^= 1
+        if self.send_op is not None:
+            gather_raw(self.send_op, q_slab, self.send_ptrs[e], None, 0)
+        self.lsa.barrier()
+        gather_raw(self.own_op, q_slab, out.data_ptr(), self.carry_ptrs[e] if self.rank > 0 else None,
+                   self.part.plane if self.rank > 0 else 0)
+        return out
+
     def exchange(self) -> None:
         ops = []
         if self.send_buf is not None:
@@ -223,6 +245,18 @@ class DistGather:
         self.exchange()
         self.gather_fn(self.own_op, q_slab, out, self.carry)
         return out
+
+
+def gather_raw(op, q: torch.Tensor, out_ptr: int, carry_ptr: int | None, ncarry: int) -> None:
+    """sb_bs6_gather_planned with raw output / carry addresses (NVLink-mapped
+    peer memory or the local halo window)."""
+    L = _lib.lib()
+    plan = op.plan()
+    if plan is None:
+        raise ValueError("the NVLink carry path needs a planned gather operator")
+    _lib.check(L.sb_bs6_gather_planned(plan.data_ptr(), op.n_blocks, op.nodes_per_block, op.row_starts.data_ptr(),
+                                       op.col_ids.data_ptr(), op.ng, op.nl, q.data_ptr(), out_ptr, carry_ptr,
+                                       ncarry, _lib.stream_handle(q.device)), "bs6_gather (NVLink carry)")
 
 
 class DistScatter:
@@ -310,10 +344,13 @@ class BenchContext:
                           "partition": "z-slabs, carry halo (BS6), one-plane halo (BS7)"}
         # per step: 7 kernels + BS6 send-plane gather (+ 3 ordered-sum kernels after the
         # NCCL all-gathers when the fused combine is not in use); NCCL p2p halos not counted
-        self.launches_per_step = 7 + 1 + (0 if self.lsa is not None else 3)
+        self.launches_per_step = 7 + 1 + (1 if self.lsa is not None else 3)  # +LSA barrier
 
     def build_slab(self, K, order, device):
         self.gather = DistGather.build(self.part, self.rank, device)
+        if self.lsa is not None:
+            self.gather.enable_lsa(self.lsa)
+            self.collective += "; BS6 carry halo written over NVLink by the send-plane gather"
         self.scat = DistScatter.build(self.part, self.rank, device)
         return _SlabInfo(self.part, self.rank)
 
@@ -340,7 +377,10 @@ class BenchContext:
                 self.reducer.combine(KN.bs5_fused_cg_update_async(1e-3, w.p, w.ap, w.x, w.r, w.cfg,
                                                                   out=w.res), out=w.res)
         elif test == "bs6":
-            self.gather.gather(w.q, w.gout)
+            if self.lsa is not None:
+                self.gather.gather_lsa(w.q, w.gout)
+            else:
+                self.gather.gather(w.q, w.gout)
         else:
             self.scat.scatter(w.ql)
 

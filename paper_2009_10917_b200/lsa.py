@@ -77,6 +77,22 @@ class LsaReducer:
         except Exception:
             pass
 
+    # ---- BS6 carry halo over NVLink (dist.DistGather.enable_lsa) ----------
+    def halo_window(self, nbytes: int) -> None:
+        """Collective: register this context's symmetric halo window."""
+        _lib.check(self.L.sb_lsa_halo_window(self.handle, int(nbytes)), "sb_lsa_halo_window")
+
+    def halo_pointers(self, offset: int, peer: int) -> tuple[int, int]:
+        """(local address, peer's NVLink-mapped address) of `offset` in the halo window."""
+        loc, rem = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(self.L.sb_lsa_halo_pointers(self.handle, int(offset), int(peer), ctypes.byref(loc),
+                                               ctypes.byref(rem)), "sb_lsa_halo_pointers")
+        return int(loc.value), int(rem.value)
+
+    def barrier(self) -> None:
+        """Collective LSA barrier on the current stream (one-thread kernel)."""
+        _lib.check(self.L.sb_lsa_barrier(self.handle, _lib.stream_handle(self.device)), "sb_lsa_barrier")
+
     # a private zeroed workspace per config (the kernels leave it zeroed)
     def _workspace(self, cfg: ReductionConfig) -> torch.Tensor:
         key = (cfg.block_size, cfg.n_blocks)

@@ -61,3 +61,39 @@ def test_lsa_inside_cuda_graph_not_required_but_stream_ordered(lsa):
     res = [lsa.bs3_norm2(x) for x in xs]
     want = [KN.bs3_norm2_async(x).item() for x in xs]
     assert [r.item() for r in res] == want
+
+
+@pytest.mark.parametrize("K,p,world", [(9, 5, 3), (8, 7, 2), (6, 1, 3)])
+def test_carry_halo_through_lsa_window_bitexact(lsa, K, p, world):
+    """The slab ranks run one after another on this GPU; each send-plane
+    gather writes through the NVLink (LSA) mapping of the halo window (peer =
+    self here), the barrier orders it, and the next rank's own gather reads
+    the carry from the window: bitwise the single-GPU gather."""
+    import paper_2009_10917_b200 as sb
+    from paper_2009_10917_b200 import dist as D
+    from paper_2009_10917_b200.mesh import build_slab_gather
+    part = D.SlabPartition(K, p, world)
+    mesh = sb.build_mesh(K, p)
+    gen = torch.Generator(device="cuda"); gen.manual_seed(K + 10 * p)
+    q = torch.empty(mesh.nl, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
+    full = sb.bs6_gather(sb.build_gather(mesh), q)
+    if not hasattr(lsa, "_halo_ok"):
+        lsa.halo_window(2 * 8 * 4_000_000)
+        lsa._halo_ok = True
+    nb = 8 * part.plane
+    for r in range(world):
+        z0, z1 = part.layers(r)
+        lo, hi = part.local_span(r)
+        c0, c1 = part.own_planes(r)
+        e = r & 1
+        carry_local, _ = lsa.halo_pointers(((r + 1) & 1) * nb, 0)   # written by rank r-1 (epoch of r-1)
+        r0, r1 = part.row_span(r)
+        out = torch.empty(r1 - r0, dtype=torch.float64, device="cuda")
+        D.gather_raw(build_slab_gather(K, p, z0, z1, c0, c1), q[lo:hi], out.data_ptr(),
+                     carry_local if r > 0 else None, part.plane if r > 0 else 0)
+        assert torch.equal(out, full[r0:r1]), r
+        sp = part.send_plane(r)
+        if sp is not None:
+            _, remote = lsa.halo_pointers(e * nb, 0)
+            D.gather_raw(build_slab_gather(K, p, z0, z1, sp, sp + 1), q[lo:hi], remote, None, 0)
+            lsa.barrier()
