@@ -330,11 +330,22 @@ class BenchContext:
             use_lsa = _nccl(None) and os.environ.get("SB200_LSA", "1") != "0"
         if use_lsa:
             from .lsa import LsaReducer, LsaUnavailable
+            why = None
             try:
                 self.lsa = LsaReducer(world, rank, device)
-                self.collective = "fused in-kernel combine over NVLink (NCCL device API, LSA window)"
             except LsaUnavailable as e:
-                self.collective += f" (fused path unavailable: {e})"
+                why = str(e)
+            # every rank must take the same path (the fused kernels are collective)
+            ok = torch.tensor([0 if self.lsa is None else 1], dtype=torch.int32, device=self.device)
+            if world > 1:
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 1:
+                self.collective = "fused in-kernel combine over NVLink (NCCL device API, LSA window)"
+            else:
+                if self.lsa is not None:
+                    self.lsa.close()
+                    self.lsa = None
+                self.collective += f" (fused path unavailable: {why or 'not on every rank'})"
         Kg = max(world, int(round(args.K * world ** (1.0 / 3.0))))
         self.part = SlabPartition(Kg, args.order, world)
         g = self.part.g
