@@ -90,6 +90,14 @@ __global__ void __launch_bounds__(256) k_bs6_rows(const int32_t *__restrict__ rs
 int bs7_lanes_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,
                      cudaStream_t st);  // sb_gs_pipe.cu
 
+// rows straight from global memory for every operator (A/B reference point)
+int bs6_rows_launch(const int32_t *rs, const int32_t *ci, int64_t ng, const double *q, double *out,
+                    const double *carry, int64_t ncarry, cudaStream_t st) {
+    const int64_t grid = std::min<int64_t>((ng + 255) / 256, (int64_t)sm_count() * 32);
+    k_bs6_rows<<<(unsigned)grid, 256, 0, st>>>(rs, ci, ng, q, out, carry, ncarry);
+    return launch_check("sb_bs6_gather");
+}
+
 }  // namespace sb
 
 using namespace sb;

@@ -305,6 +305,9 @@ __global__ void __launch_bounds__(T, MINB) k_bs6_lanes(const int32_t *__restrict
     }
 }
 
+int bs6_rows_launch(const int32_t *rs, const int32_t *ci, int64_t ng, const double *q, double *out,
+                    const double *carry, int64_t ncarry, cudaStream_t st);  // sb_gs.cu
+
 static int64_t bs6_G(int64_t npb) { return std::max<int64_t>(1, kBs6Cap / npb); }
 
 }  // namespace sb
@@ -369,6 +372,8 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     else if (5 * nl >= 11 * ng) { pairs = false; sw = true; mb = 8; }
     else { pairs = false; sw = false; mb = 10; }
     static const char *cfg = getenv("SB200_BS6_CFG");
+    if (cfg && cfg[0] == 'r' && cfg[1] == 'o' && cfg[2] == 'w' && cfg[3] == 's')
+        return bs6_rows_launch(rs, ci, ng, q, out, carry, ncarry, as_stream(s));
     if (cfg) {
         pairs = cfg[0] == 'p';
         const char *c1 = strchr(cfg, ',');
