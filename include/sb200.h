@@ -124,6 +124,14 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t n_blocks, int64_t nodes_p
 int sb_bs7_scatter(const int32_t *ids, int64_t nl, const double *q_global, int64_t ng,
                    double *q_local, int has_mask, sb_stream_t stream);
 
+/* gs.py:42-61 with q_global in two pieces: ids < n_own read q_own[id], ids
+ * >= n_own read q_halo[id - n_own] (a multi-GPU slab's own rows and the halo
+ * plane another rank wrote over NVLink; dist.py).  Ids must be < n_own +
+ * n_halo (not re-checked). */
+int sb_bs7_scatter_split(const int32_t *ids, int64_t nl, const double *q_own, int64_t n_own,
+                         const double *q_halo, int64_t n_halo, double *q_local, int has_mask,
+                         sb_stream_t stream);
+
 /* ---- operator construction (mesh.py:73-153) ------------------------------
  * Slab form: elements with ez in [z0, z1) of the K^3 order-p mesh; the
  * single-GPU operator is z0 = 0, z1 = K.  Local indices are relative to the

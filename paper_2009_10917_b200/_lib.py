@@ -50,6 +50,7 @@ _SIGS = {
     "sb_bs6_gather": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp,
                                _c_vp, _c_i64, _c_vp]),
     "sb_bs7_scatter": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_int, _c_vp]),
+    "sb_bs7_scatter_split": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_int, _c_vp]),
     "sb_build_l2g": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp]),
     "sb_build_gather_csr": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp,
                                      _c_vp, _c_vp]),

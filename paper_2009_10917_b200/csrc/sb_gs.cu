@@ -89,6 +89,8 @@ __global__ void __launch_bounds__(256) k_bs6_rows(const int32_t *__restrict__ rs
 
 int bs7_lanes_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,
                      cudaStream_t st);  // sb_gs_pipe.cu
+int bs7_split_launch(const int32_t *ids, int64_t nl, const double *qg, int32_t split, const double *qh,
+                     double *ql, int has_mask, cudaStream_t st);  // sb_gs_pipe.cu
 
 // rows straight from global memory for every operator (A/B reference point)
 int bs6_rows_launch(const int32_t *rs, const int32_t *ci, int64_t ng, const double *q, double *out,
@@ -137,6 +139,18 @@ int sb_bs7_scatter(const int32_t *ids, int64_t nl, const double *qg, int64_t ng,
     }
     if (nl == 0) return SB_OK;
     return bs7_lanes_launch(ids, nl, qg, ql, has_mask, as_stream(s));
+}
+
+int sb_bs7_scatter_split(const int32_t *ids, int64_t nl, const double *q_own, int64_t n_own,
+                         const double *q_halo, int64_t n_halo, double *ql, int has_mask, sb_stream_t s) {
+    clear_error();
+    if (nl < 0 || n_own < 0 || n_halo < 0 || n_own > 0x7fffffffLL ||
+        (nl > 0 && (!ids || !ql || (n_own > 0 && !q_own) || (n_halo > 0 && !q_halo)))) {
+        set_error("sb_bs7_scatter_split: invalid arguments");
+        return SB_E_INVALID;
+    }
+    if (nl == 0) return SB_OK;
+    return bs7_split_launch(ids, nl, q_own, (int32_t)n_own, q_halo, ql, has_mask, as_stream(s));
 }
 
 }  // extern "C"

@@ -40,9 +40,13 @@ constexpr int kBs6MinCtas = 12;
 // local entries (ids: one 128 B row; gathers: ~32/(p+1)+1 element-edge runs;
 // stores: two 128 B rows), where the int4 kernel above spreads a warp over
 // 128 entries and pays more L1 tag lookups per instruction.
-template <int T, int U, bool MASK>
+// SPLIT: q_global lives in two pieces -- ids < split index `qg`, ids >= split
+// index `qh` (the multi-GPU slab's own rows and the halo plane written over
+// NVLink by the rank above, dist.py DistScatter.enable_lsa).
+template <int T, int U, bool MASK, bool SPLIT = false>
 __global__ void __launch_bounds__(T) k_bs7_lanes(const int32_t *__restrict__ ids, int64_t nl,
-                                                const double *__restrict__ qg, double *__restrict__ ql) {
+                                                const double *__restrict__ qg, double *__restrict__ ql,
+                                                int32_t split = 0, const double *__restrict__ qh = nullptr) {
     const uint64_t pol = policy_evict_last();
     const int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x;
     int32_t d[U];
@@ -52,10 +56,22 @@ __global__ void __launch_bounds__(T) k_bs7_lanes(const int32_t *__restrict__ ids
     double v[U];
 #pragma unroll
     for (int j = 0; j < U; j++)
-        if (base + j * T < nl && (!MASK || d[j] >= 0)) v[j] = ld_keep(qg + d[j], pol);
+        if (base + j * T < nl && (!MASK || d[j] >= 0))
+            v[j] = (!SPLIT || d[j] < split) ? ld_keep(qg + d[j], pol) : ld_keep(qh + (d[j] - split), pol);
 #pragma unroll
     for (int j = 0; j < U; j++)
         if (base + j * T < nl && (!MASK || d[j] >= 0)) st_stream(ql + base + j * T, v[j]);
+}
+
+int bs7_split_launch(const int32_t *ids, int64_t nl, const double *qg, int32_t split, const double *qh,
+                     double *ql, int has_mask, cudaStream_t st) {
+    constexpr int T = 128, U = 4;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, (nl + T * U - 1) / (T * U));
+    if (has_mask)
+        k_bs7_lanes<T, U, true, true><<<grid, T, 0, st>>>(ids, nl, qg, ql, split, qh);
+    else
+        k_bs7_lanes<T, U, false, true><<<grid, T, 0, st>>>(ids, nl, qg, ql, split, qh);
+    return launch_check("sb_bs7_scatter_split");
 }
 
 int bs7_lanes_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,

@@ -208,16 +208,15 @@ class DistGather:
                                                          nodes_per_block, device)
         return cls(part, rank, own, send, device, group=group)
 
-    def enable_lsa(self, lsa) -> None:
-        """Collective: carry halo over NVLink peer memory (lsa.LsaReducer).
-        The send-plane gather then writes its partials straight into rank+1's
-        carry buffer (two buffers, alternating per call) and one LSA barrier
-        replaces the NCCL send/recv pair."""
+    def enable_lsa(self, lsa, offset: int = 0) -> None:
+        """Carry halo over NVLink peer memory (lsa.LsaReducer whose halo window
+        holds 2 planes at byte `offset`).  The send-plane gather then writes its
+        partials straight into rank+1's carry buffer (two buffers, alternating
+        per call) and one LSA barrier replaces the NCCL send/recv pair."""
         nb = 8 * self.part.plane
-        lsa.halo_window(2 * nb)
         self.lsa, self.epoch = lsa, 0
-        self.carry_ptrs = [lsa.halo_pointers(e * nb, self.rank)[0] for e in (0, 1)]
-        self.send_ptrs = ([lsa.halo_pointers(e * nb, self.rank + 1)[1] for e in (0, 1)]
+        self.carry_ptrs = [lsa.halo_pointers(offset + e * nb, self.rank)[0] for e in (0, 1)]
+        self.send_ptrs = ([lsa.halo_pointers(offset + e * nb, self.rank + 1)[1] for e in (0, 1)]
                           if self.send_op is not None else None)
 
     def gather_lsa(self, q_slab: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
@@ -294,6 +293,36 @@ class DistScatter:
         self.exchange()
         self.scatter_fn(self.ids, self.window, q_local)
 
+    def enable_lsa(self, lsa, offset: int) -> None:
+        """One-plane halo over NVLink: rank r+1 writes its bottom plane into
+        rank r's halo buffer (2 planes at byte `offset` of the LSA halo window,
+        alternating per call), one LSA barrier, then a split scatter reads the
+        own rows from `window` and the halo plane from the LSA buffer."""
+        nb = 8 * self.part.plane
+        self.lsa, self.epoch = lsa, 0
+        self.halo_ptrs = ([lsa.halo_pointers(offset + e * nb, self.rank)[0] for e in (0, 1)]
+                          if self.rank < self.part.world - 1 else None)
+        self.down_ptrs = ([lsa.halo_pointers(offset + e * nb, self.rank - 1)[1] for e in (0, 1)]
+                          if self.rank > 0 else None)
+
+    def scatter_lsa(self, q_local: torch.Tensor) -> None:
+        L = _lib.lib()
+        e = self.epoch
+        self.epoch ^= 1
+        st = _lib.stream_handle(self.device)
+        plane = self.part.plane
+        if self.down_ptrs is not None:  # my bottom plane -> rank-1's halo buffer, over NVLink
+            _lib.check(L.sb_bs1_copy(self.window.data_ptr(), self.down_ptrs[e], plane, st), "bs7 halo put")
+        self.lsa.barrier()
+        nl = int(self.ids.shape[0])
+        if self.halo_ptrs is None:  # last rank owns its top plane
+            _lib.check(L.sb_bs7_scatter(self.ids.data_ptr(), nl, self.window.data_ptr(),
+                                        int(self.window.shape[0]), q_local.data_ptr(), 0, st), "bs7_scatter")
+        else:
+            _lib.check(L.sb_bs7_scatter_split(self.ids.data_ptr(), nl, self.window.data_ptr(), self.own_rows,
+                                              self.halo_ptrs[e], plane, q_local.data_ptr(), 0, st),
+                       "bs7_scatter_split")
+
 
 def _gpu_scatter(ids: torch.Tensor, window: torch.Tensor, q_local: torch.Tensor) -> None:
     from .gs import bs7_scatter
@@ -353,16 +382,21 @@ class BenchContext:
                           "nl_global": Kg ** 3 * (args.order + 1) ** 3,
                           "slab_layers": [self.part.layers(r) for r in range(world)],
                           "partition": "z-slabs, carry halo (BS6), one-plane halo (BS7)"}
-        # per step: 7 kernels + BS6 send-plane gather (+ 3 ordered-sum kernels after the
-        # NCCL all-gathers when the fused combine is not in use); NCCL p2p halos not counted
-        self.launches_per_step = 7 + 1 + (1 if self.lsa is not None else 3)  # +LSA barrier
+        # our launches per step: the 7 tests + BS6's send-plane gather, plus either the
+        # NVLink path's 2 LSA barriers and BS7 halo put, or the 3 ordered sums after the
+        # NCCL all-gathers (NCCL's own kernels not counted)
+        self.launches_per_step = 7 + 1 + 3
 
     def build_slab(self, K, order, device):
         self.gather = DistGather.build(self.part, self.rank, device)
-        if self.lsa is not None:
-            self.gather.enable_lsa(self.lsa)
-            self.collective += "; BS6 carry halo written over NVLink by the send-plane gather"
         self.scat = DistScatter.build(self.part, self.rank, device)
+        if self.lsa is not None:
+            nb = 8 * self.part.plane
+            self.lsa.halo_window(4 * nb)  # [BS6 carry x2 | BS7 halo x2]
+            self.gather.enable_lsa(self.lsa, 0)
+            self.scat.enable_lsa(self.lsa, 2 * nb)
+            self.collective += ("; BS6 carry and BS7 halo planes written over NVLink into the peer's "
+                                "window + LSA barrier")
         return _SlabInfo(self.part, self.rank)
 
     def call(self, w, test):
@@ -392,6 +426,8 @@ class BenchContext:
                 self.gather.gather_lsa(w.q, w.gout)
             else:
                 self.gather.gather(w.q, w.gout)
+        elif self.lsa is not None:
+            self.scat.scatter_lsa(w.ql)
         else:
             self.scat.scatter(w.ql)
 

@@ -97,3 +97,45 @@ def test_carry_halo_through_lsa_window_bitexact(lsa, K, p, world):
             _, remote = lsa.halo_pointers(e * nb, 0)
             D.gather_raw(build_slab_gather(K, p, z0, z1, sp, sp + 1), q[lo:hi], remote, None, 0)
             lsa.barrier()
+
+
+@pytest.mark.parametrize("K,p,world", [(7, 3, 3), (6, 7, 2), (5, 1, 4)])
+def test_bs7_halo_through_lsa_window_bitexact(lsa, K, p, world):
+    """BS7 over slabs with the one-plane halo put through the LSA mapping of
+    the halo window (peer = self) and the split scatter (own rows + halo)."""
+    import paper_2009_10917_b200 as sb
+    from paper_2009_10917_b200 import _lib
+    from paper_2009_10917_b200 import dist as D
+    from paper_2009_10917_b200.mesh import build_slab_l2g
+    part = D.SlabPartition(K, p, world)
+    mesh = sb.build_mesh(K, p)
+    gen = torch.Generator(device="cuda"); gen.manual_seed(3 * K + p)
+    qg = torch.empty(mesh.ng, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
+    want = qg[mesh.local_to_global.long()]
+    if not hasattr(lsa, "_halo_ok"):
+        lsa.halo_window(2 * 8 * 4_000_000)
+        lsa._halo_ok = True
+    L = _lib.lib()
+    st = _lib.stream_handle()
+    plane = part.plane
+    for r in range(world):
+        z0, z1 = part.layers(r)
+        lo, hi = part.local_span(r)
+        a, b = part.read_span(r)
+        ids = build_slab_l2g(K, p, z0, z1) - a
+        ql = torch.zeros(hi - lo, dtype=torch.float64, device="cuda")
+        if r < world - 1:
+            own = part.ng_own(r)
+            a1, _ = part.read_span(r + 1)
+            loc, rem = lsa.halo_pointers((r & 1) * 8 * plane, 0)
+            src = qg[a1:a1 + plane].clone()   # rank r+1's bottom plane
+            _lib.check(L.sb_bs1_copy(src.data_ptr(), rem, plane, st), "put")
+            lsa.barrier()
+            win = qg[a:a + own].clone()
+            _lib.check(L.sb_bs7_scatter_split(ids.data_ptr(), ids.shape[0], win.data_ptr(), own, loc, plane,
+                                              ql.data_ptr(), 0, st), "split")
+        else:
+            win = qg[a:b].clone()
+            _lib.check(L.sb_bs7_scatter(ids.data_ptr(), ids.shape[0], win.data_ptr(), win.shape[0],
+                                        ql.data_ptr(), 0, st), "scatter")
+        assert torch.equal(ql, want[lo:hi]), r
