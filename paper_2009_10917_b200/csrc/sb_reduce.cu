@@ -38,6 +38,10 @@ namespace sb {
 #define SB_RING_DOT 32768
 #define SB_RING_FUSED 32768
 #endif
+#ifndef SB_BPC
+#define SB_BPC 1
+#endif
+constexpr int kBpc = SB_BPC;  // lattice blocks per CTA for block_size 256 (A/B)
 constexpr int kSpsNorm = SB_SPS_NORM, kSpsDot = SB_SPS_DOT, kSpsFused = SB_SPS_FUSED;
 constexpr int kRingNorm = SB_RING_NORM, kRingDot = SB_RING_DOT, kRingFused = SB_RING_FUSED;
 
@@ -240,7 +244,7 @@ struct NArr {
     static constexpr int v = MODE == R_NORM ? 1 : (MODE == R_DOT ? 2 : 4);
 };
 
-template <int T, int SPT, int MODE, int ST, int SPS>
+template <int T, int SPT, int MODE, int ST, int SPS, int BPC = 1>
 __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs Ain) {
     RArgs A = Ain;
     if (!resolve(A)) return;
@@ -348,43 +352,48 @@ __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs Ain) {
         for (int j = 0; j < SPT; j++) sm[tid + j * T] = acc[j];
     }
     __syncthreads();
-    // tree fold (threads >= T skip the smem levels; warp 0 does the shuffles)
-    for (int k = BS / 2; k >= 32; k >>= 1) {
-        for (int s = tid; s < k; s += T) sm[s] = add(sm[s], sm[s + k]);
+    // tree fold of each of the CTA's BPC lattice blocks (LB slots each):
+    // threads >= T skip the smem levels; warp h does block h's shuffles
+    constexpr int LB = BS / BPC;
+    for (int k = LB / 2; k >= 32; k >>= 1) {
+        for (int s = tid; s < BPC * k; s += T) {
+            const int h = s / k, i = s - h * k;
+            sm[h * LB + i] = add(sm[h * LB + i], sm[h * LB + i + k]);
+        }
         __syncthreads();
     }
     double v = 0.0;
-    if (tid < 32) {
-        constexpr int W = BS < 32 ? BS : 32;
-        if (tid < W) v = sm[tid];
+    if (warp < BPC) {
+        constexpr int W = LB < 32 ? LB : 32;
+        if (lane < W) v = sm[warp * LB + lane];
         for (int off = W / 2; off >= 1; off >>= 1) v = add(v, __shfl_down_sync(0xffffffffu, v, off));
+        if (lane == 0) {
+            A.partials[(int64_t)blockIdx.x * BPC + warp] = v;
+            __threadfence();  // visible before this CTA's ticket
+        }
     }
     __syncthreads();
     // second stage by the last CTA
     __shared__ bool is_last;
     if (tid == 0) {
-        A.partials[blockIdx.x] = v;
         __threadfence();
         is_last = atomicAdd(A.ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    if (tid < T) {
-        for (int j = 0; j < SPT; j++) {
-            const int t = tid + j * T;
-            double a2 = 0.0;
-            for (int64_t c = t; c < A.nb; c += BS) a2 = add(a2, __ldcg(A.partials + c));
-            sm[t] = a2;
-        }
+    for (int t = tid; t < LB; t += T) {
+        double a2 = 0.0;
+        for (int64_t c = t; c < A.nb; c += LB) a2 = add(a2, __ldcg(A.partials + c));
+        sm[t] = a2;
     }
     __syncthreads();
-    for (int k = BS / 2; k >= 32; k >>= 1) {
+    for (int k = LB / 2; k >= 32; k >>= 1) {
         for (int s = tid; s < k; s += T) sm[s] = add(sm[s], sm[s + k]);
         __syncthreads();
     }
     if (tid < 32) {
-        constexpr int W = BS < 32 ? BS : 32;
+        constexpr int W = LB < 32 ? LB : 32;
         double r = tid < W ? sm[tid] : 0.0;
         for (int off = W / 2; off >= 1; off >>= 1) r = add(r, __shfl_down_sync(0xffffffffu, r, off));
         if (tid == 0) {
@@ -482,12 +491,12 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
         // ring shape (stages x steps per stage): ~32-48 KB of stages per CTA
         constexpr int SPS = MODE == R_NORM ? kSpsNorm : (MODE == R_DOT ? kSpsDot : kSpsFused);
         constexpr int RING = MODE == R_NORM ? kRingNorm : (MODE == R_DOT ? kRingDot : kRingFused);
-#define SB_TMA(T_, SPT_)                                                                                  \
+#define SB_TMA_B(T_, SPT_, BPC_)                                                                          \
     {                                                                                                     \
         constexpr int SPS_ = ring_sps(SPS, T_ * SPT_);                                                   \
         constexpr int STB_ = SPS_ * NA * T_ * SPT_ * 8;                                                  \
         constexpr int ST_ = ring_stages(RING, STB_);                                                      \
-        auto kern = k_lattice_tma<T_, SPT_, MODE, ST_, SPS_>;                                             \
+        auto kern = k_lattice_tma<T_, SPT_, MODE, ST_, SPS_, BPC_>;                                       \
         static int attr_dev = -1; /* per instantiation and device */                                      \
         int dev = 0;                                                                                      \
         cudaGetDevice(&dev);                                                                              \
@@ -498,14 +507,18 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
                 return rc;                                                                                \
             attr_dev = dev;                                                                               \
         }                                                                                                 \
-        kern<<<grid, T_ + 32, ST_ * STB_, st>>>(A);                                                       \
+        kern<<<grid / BPC_, T_ + 32, ST_ * STB_, st>>>(A);                                                \
     }
+#define SB_TMA(T_, SPT_) SB_TMA_B(T_, SPT_, 1)
         switch (A.bs) {
             case 64: SB_TMA(64, 1); break;
             case 128: SB_TMA(128, 1); break;
-            case 256: SB_TMA(256, 1); break;
+            case 256:
+                if (kBpc == 2 && (A.nb & 1) == 0) SB_TMA_B(256, 2, 2) else SB_TMA(256, 1);
+                break;
             default: SB_TMA(256, 2); break;
         }
+#undef SB_TMA_B
 #undef SB_TMA
         return launch_check(name);
     }
