@@ -487,7 +487,13 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
     // TMA ring: ~32 KB of stages per CTA (so <= 4 CTAs/SM by shared memory)
     constexpr int NA = NArr<MODE>::v;
     const bool tma_ok = aligned16(A.u) && aligned16(A.v) && (MODE != R_FUSED || (aligned16(A.x) && aligned16(A.r)));
-    if (tma_ok && use_tma() && (A.bs == 64 || A.bs == 128 || A.bs == 256 || A.bs == 512)) {
+    // Below a few MB per array the register-pipelined lattice has the lower
+    // fixed cost (graph-timed T0 5.7 vs 6.2 us for BS3, 4.9 vs 6.3 for BS4, 6.5
+    // vs 7.5 for BS5) and wins while the data is L2-resident; from ~1e7 DOFs
+    // the TMA ring streams faster (profiles/r01_model_fit.md).  Same lattice,
+    // bitwise the same scalar either way.
+    constexpr int64_t kTmaMinN = MODE == R_FUSED ? 3000000 : 6000000;
+    if (tma_ok && use_tma() && A.n >= kTmaMinN && (A.bs == 64 || A.bs == 128 || A.bs == 256 || A.bs == 512)) {
         // ring shape (stages x steps per stage): ~32-48 KB of stages per CTA
         constexpr int SPS = MODE == R_NORM ? kSpsNorm : (MODE == R_DOT ? kSpsDot : kSpsFused);
         constexpr int RING = MODE == R_NORM ? kRingNorm : (MODE == R_DOT ? kRingDot : kRingFused);

@@ -232,6 +232,29 @@ def test_large_n_bitwise_vs_oracle(sb, oracle, n):
         oracle.set_threads(1)
 
 
+@pytest.mark.parametrize("n", [6_000_000, 6_000_001, 7_340_033, 12_582_917])
+def test_tma_ring_sizes_and_configs_vs_oracle(sb, oracle, n):
+    """The TMA-ring lattice (taken from 3-6 M elements on) at ragged sizes:
+    leftover chain steps that do not fill a stage, a partial last chunk, and
+    block sizes 64..512 -- bitwise the lattice oracle."""
+    oracle.set_threads(oracle.max_threads())
+    try:
+        rng = np.random.default_rng([n, 5])
+        xh, yh = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+        x, y = d(xh), d(yh)
+        for bs, nb in ((64, 7), (128, 33), (256, 512), (512, 296), (256, 1184), (256, 3)):
+            cfg = sb.ReductionConfig(bs, nb)
+            assert sb.bs3_norm2(x, cfg) == oracle.bs3_norm2(xh, bs, nb), (bs, nb)
+            assert sb.bs4_dot(x, y, cfg) == oracle.bs4_dot(xh, yh, bs, nb), (bs, nb)
+            xo, ro = xh.copy(), yh.copy()
+            want = oracle.bs5_fused_cg_update(0.375, yh, xh, xo, ro, bs, nb)
+            xx, rr = x.clone(), y.clone()
+            assert sb.bs5_fused_cg_update(0.375, y, x, xx, rr, cfg) == want, (bs, nb)
+            assert np.array_equal(h(xx), xo) and np.array_equal(h(rr), ro)
+    finally:
+        oracle.set_threads(1)
+
+
 def test_fallback_kernels_match(sb):
     """The register-unrolled lattice and one-tile-per-CTA gather/scatter kernels
     (SB200_NO_TMA / SB200_NO_PIPE) must agree bitwise with the fast paths."""
