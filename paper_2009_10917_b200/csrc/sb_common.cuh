@@ -58,6 +58,16 @@ int cg_reduce(int mode, const double *u, const double *v, double *x, double *r, 
               int64_t nb, void *ws, double *result, const int32_t *gate, const double *alpha,
               cudaStream_t st, const char *name);
 
+// Completion ticket of single-launch reductions: a gpu-scope acq_rel add.  The
+// release publishes this CTA's partials (written before the preceding
+// __syncthreads, cumulative through the barrier); the acquire in the last CTA
+// orders its reads of every other CTA's partials -- no separate fences.
+__device__ __forceinline__ unsigned ticket_add(unsigned *t) {
+    unsigned prev;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(t) : "memory");
+    return prev;
+}
+
 // ---- cache-policy helpers: HBM streams are touched once -> evict-first.
 __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ld_stream(const double2 *p) { return __ldcs(p); }

@@ -160,13 +160,10 @@ __device__ __forceinline__ void second_stage(const RArgs &A, double *sm, int bs,
     __shared__ bool is_last;
     if (threadIdx.x == 0) {
         A.partials[blockIdx.x] = v;
-        __threadfence();
-        const unsigned prev = atomicAdd(A.ticket, 1u);
-        is_last = (prev == gridDim.x - 1);
+        is_last = ticket_add(A.ticket) == gridDim.x - 1;
     }
     __syncthreads();
     if (!is_last) return;
-    __threadfence();
     // _final_reduce (kernels.py:72-81): s[t] = 0.0 + partials[t] + partials[t+bs] + ...
     for (int j = 0; j < spt; j++) {
         const int t = threadIdx.x + j * T;
@@ -367,21 +364,15 @@ __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs Ain) {
         constexpr int W = LB < 32 ? LB : 32;
         if (lane < W) v = sm[warp * LB + lane];
         for (int off = W / 2; off >= 1; off >>= 1) v = add(v, __shfl_down_sync(0xffffffffu, v, off));
-        if (lane == 0) {
-            A.partials[(int64_t)blockIdx.x * BPC + warp] = v;
-            __threadfence();  // visible before this CTA's ticket
-        }
+        if (lane == 0) A.partials[(int64_t)blockIdx.x * BPC + warp] = v;
     }
     __syncthreads();
-    // second stage by the last CTA
+    // second stage by the last CTA (ticket_add: release of the partials above,
+    // acquire of everyone else's in the last CTA)
     __shared__ bool is_last;
-    if (tid == 0) {
-        __threadfence();
-        is_last = atomicAdd(A.ticket, 1u) == gridDim.x - 1;
-    }
+    if (tid == 0) is_last = ticket_add(A.ticket) == gridDim.x - 1;
     __syncthreads();
     if (!is_last) return;
-    __threadfence();
     for (int t = tid; t < LB; t += T) {
         double a2 = 0.0;
         for (int64_t c = t; c < A.nb; c += LB) a2 = add(a2, __ldcg(A.partials + c));
