@@ -41,6 +41,7 @@ namespace sb {
 #ifndef SB_BPC
 #define SB_BPC 1
 #endif
+
 constexpr int kBpc = SB_BPC;  // lattice blocks per CTA for block_size 256 (A/B)
 constexpr int kSpsNorm = SB_SPS_NORM, kSpsDot = SB_SPS_DOT, kSpsFused = SB_SPS_FUSED;
 constexpr int kRingNorm = SB_RING_NORM, kRingDot = SB_RING_DOT, kRingFused = SB_RING_FUSED;
