@@ -45,6 +45,10 @@ namespace sb {
 constexpr int kBpc = SB_BPC;  // lattice blocks per CTA for block_size 256 (A/B)
 constexpr int kSpsNorm = SB_SPS_NORM, kSpsDot = SB_SPS_DOT, kSpsFused = SB_SPS_FUSED;
 constexpr int kRingNorm = SB_RING_NORM, kRingDot = SB_RING_DOT, kRingFused = SB_RING_FUSED;
+#ifndef SB_RING_FUSED_BPC4
+#define SB_RING_FUSED_BPC4 131072
+#endif
+constexpr int kRingFusedBpc4 = SB_RING_FUSED_BPC4;  // 4 stages of 4 arrays x 8 KB
 
 enum RMode { R_NORM = 0, R_DOT = 1, R_FUSED = 2 };
 
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs Ain) {
     // threads >= T skip the smem levels; warp h does block h's shuffles
     constexpr int LB = BS / BPC;
     for (int k = LB / 2; k >= 32; k >>= 1) {
-        for (int s = tid; s < BPC * k; s += T) {
+        for (int s = tid; s < BPC * k && tid < T; s += T) {  // (the producer warp has tid >= T)
             const int h = s / k, i = s - h * k;
             sm[h * LB + i] = add(sm[h * LB + i], sm[h * LB + i + k]);
         }
@@ -489,11 +493,11 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
         // ring shape (stages x steps per stage): ~32-48 KB of stages per CTA
         constexpr int SPS = MODE == R_NORM ? kSpsNorm : (MODE == R_DOT ? kSpsDot : kSpsFused);
         constexpr int RING = MODE == R_NORM ? kRingNorm : (MODE == R_DOT ? kRingDot : kRingFused);
-#define SB_TMA_B(T_, SPT_, BPC_)                                                                          \
+#define SB_TMA_BR(T_, SPT_, BPC_, RING_)                                                                  \
     {                                                                                                     \
         constexpr int SPS_ = ring_sps(SPS, T_ * SPT_);                                                   \
         constexpr int STB_ = SPS_ * NA * T_ * SPT_ * 8;                                                  \
-        constexpr int ST_ = ring_stages(RING, STB_);                                                      \
+        constexpr int ST_ = ring_stages(RING_, STB_);                                                     \
         auto kern = k_lattice_tma<T_, SPT_, MODE, ST_, SPS_, BPC_>;                                       \
         static int attr_dev = -1; /* per instantiation and device */                                      \
         int dev = 0;                                                                                      \
@@ -507,16 +511,24 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
         }                                                                                                 \
         kern<<<grid / BPC_, T_ + 32, ST_ * STB_, st>>>(A);                                                \
     }
+#define SB_TMA_B(T_, SPT_, BPC_) SB_TMA_BR(T_, SPT_, BPC_, RING)
 #define SB_TMA(T_, SPT_) SB_TMA_B(T_, SPT_, 1)
         switch (A.bs) {
             case 64: SB_TMA(64, 1); break;
             case 128: SB_TMA(128, 1); break;
             case 256:
-                if (kBpc == 2 && (A.nb & 1) == 0) SB_TMA_B(256, 2, 2) else SB_TMA(256, 1);
+                // BS5: four lattice blocks per CTA (8 KB chunks per array per step,
+                // one 128 KB ring per SM) -- +4-5% over one block per CTA, whose 2 KB
+                // chunks write back less efficiently (profiles/r01_lattice_variants.md);
+                // BS3/BS4 (read-only) keep one block per CTA.
+                if (MODE == R_FUSED && (A.nb & 3) == 0) SB_TMA_BR(256, 4, 4, kRingFusedBpc4)
+                else if (kBpc == 2 && (A.nb & 1) == 0) SB_TMA_B(256, 2, 2)
+                else SB_TMA(256, 1);
                 break;
             default: SB_TMA(256, 2); break;
         }
 #undef SB_TMA_B
+#undef SB_TMA_BR
 #undef SB_TMA
         return launch_check(name);
     }
