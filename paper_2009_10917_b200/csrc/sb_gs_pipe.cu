@@ -399,14 +399,15 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     }
 #define SB_PICK(K_, MB_) (sw ? K_<T, kBs6Cap, true, MB_> : K_<T, kBs6Cap, false, MB_>)
 #define SB_PICK_MB(K_) (mb == 6 ? SB_PICK(K_, 6) : mb == 8 ? SB_PICK(K_, 8) : mb == 10 ? SB_PICK(K_, 10) : SB_PICK(K_, 12))
+    auto grid_for = [&](const void *k) {
+        int per_sm = 1;  // (8 KB of dynamic shared memory: below the default limit)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, T, smem);
+        return (unsigned)std::max<int64_t>(1, std::min<int64_t>(nsb, (int64_t)sm_count() * std::max(1, per_sm)));
+    };
     const KernT kern = pairs ? SB_PICK_MB(k_bs6_pairs) : SB_PICK_MB(k_bs6_lanes);
+    kern<<<grid_for((const void *)kern), T, smem, as_stream(s)>>>(plan, nsb, rs, ci, q, out, carry, ncarry);
 #undef SB_PICK_MB
 #undef SB_PICK
-    int per_sm = 1;  // (8 KB of dynamic shared memory: below the default limit)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
-    const int64_t grid = std::min<int64_t>(nsb, (int64_t)sm_count() * std::max(1, per_sm));
-    kern<<<(unsigned)std::max<int64_t>(1, grid), T, smem, as_stream(s)>>>(plan, nsb, rs, ci, q, out, carry,
-                                                                          ncarry);
     return launch_check("sb_bs6_gather_planned");
 }
 

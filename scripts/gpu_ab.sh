@@ -1,4 +1,6 @@
 set -x
-rm -f gpurun_out/bs6_ab12.log
-for c in lanes,0,12 lanes,1,12 lanes,0,10 lanes,1,10 lanes,0,8 lanes,1,8 lanes,1,6 lanes,0,6; do SB200_BS6_CFG=$c timeout 300 python scripts/expt/time_bs6.py 3 4 >> gpurun_out/bs6_ab12.log 2>&1; done
-cat gpurun_out/bs6_ab12.log
+rm -f gpurun_out/bs6_run.log
+SB200_BS6_RUN=16 timeout 600 python -m pytest tests/test_gpu_gs.py -q -x -p no:cacheprovider 2>&1 | tail -2 >> gpurun_out/bs6_run.log
+SB200_BS6_RUN=0 timeout 600 python -m pytest tests/test_gpu_gs.py -q -x -p no:cacheprovider 2>&1 | tail -2 >> gpurun_out/bs6_run.log
+for r in 1 2 4 16 64 0; do echo "run=$r" >> gpurun_out/bs6_run.log; SB200_BS6_RUN=$r timeout 300 python scripts/expt/time_bs6.py 2 3 5 7 15 >> gpurun_out/bs6_run.log 2>&1; done
+cat gpurun_out/bs6_run.log
