@@ -354,7 +354,9 @@ class BenchContext:
         # BS3/BS4/BS5: the reduction and the cross-rank combine fused in one
         # kernel over NVLink peer memory (lsa.py) when every rank is an LSA
         # peer; otherwise (or SB200_LSA=0) NCCL all-gather + ordered sum.
-        self.lsa, self.collective = None, "nccl all_gather + sb_sum_ordered"
+        self.lsa = None
+        self.collective = ("nccl" if _nccl(None) else "gloo (host-staged)") + \
+            " all_gather + sb_sum_ordered; BS6/BS7 halos by send/recv"
         if use_lsa is None:
             use_lsa = _nccl(None) and os.environ.get("SB200_LSA", "1") != "0"
         if use_lsa:
