@@ -261,6 +261,17 @@ int sb_lsa_destroy(sb_lsa_t *ctx);
 int sb_lsa_halo_window(sb_lsa_t *ctx, size_t bytes);
 int sb_lsa_halo_pointers(sb_lsa_t *ctx, size_t offset, int peer, void **local, void **remote);
 int sb_lsa_barrier(sb_lsa_t *ctx, sb_stream_t stream);
+/* Multi-GPU device-resident CG: sb_cg_pap / sb_cg_update whose reductions
+ * (pAp, r.r) combine over the ranks in the same launch, so every rank's
+ * sb_cg_state holds the global scalars and the ranks gate identically;
+ * sb_cg_begin / sb_cg_direction are used unchanged (with rr0 / b.b from
+ * sb_lsa_bs3_norm2).  Vectors are the rank's chunks. */
+int sb_lsa_cg_pap(const double *p, const double *ap, int64_t n, int64_t block_size,
+                  int64_t n_blocks, void *workspace, sb_cg_state *state, sb_lsa_t *ctx,
+                  sb_stream_t stream);
+int sb_lsa_cg_update(int fused, const double *p, const double *ap, double *x, double *r,
+                     int64_t n, int64_t block_size, int64_t n_blocks, void *workspace,
+                     sb_cg_state *state, sb_lsa_t *ctx, sb_stream_t stream);
 int sb_lsa_bs3_norm2(const double *x, int64_t n, int64_t block_size, int64_t n_blocks,
                      void *workspace, double *result, sb_lsa_t *ctx, sb_stream_t stream);
 int sb_lsa_bs4_dot(const double *x, const double *y, int64_t n, int64_t block_size,

@@ -75,6 +75,9 @@ _SIGS = {
     "sb_lsa_halo_window": (_c_int, [_c_vp, _c_size]),
     "sb_lsa_halo_pointers": (_c_int, [_c_vp, _c_size, _c_int, _c_vp, _c_vp]),
     "sb_lsa_barrier": (_c_int, [_c_vp, _c_vp]),
+    "sb_lsa_cg_pap": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "sb_lsa_cg_update": (_c_int, [_c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp,
+                                  _c_vp, _c_vp]),
     "sb_lsa_bs3_norm2": (_c_int, [_c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
     "sb_lsa_bs4_dot": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
     "sb_lsa_bs5_fused_cg_update": (_c_int, [_c_dbl, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64,

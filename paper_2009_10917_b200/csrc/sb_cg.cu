@@ -71,6 +71,36 @@ __global__ void k_cg_advance(sb_cg_state *st) {
     }
 }
 
+int cg_pap_impl(const double *p, const double *ap, int64_t n, int64_t bs, int64_t nb, void *ws,
+                sb_cg_state *st, const LsaArgs *lsa, cudaStream_t cs) {
+    if (!st) {
+        set_error("sb_cg_pap: null state");
+        return SB_E_INVALID;
+    }
+    if (int rc = cg_reduce(1, p, ap, nullptr, nullptr, n, bs, nb, ws, &st->pap, &st->active, nullptr, cs,
+                           "sb_cg_pap", lsa))
+        return rc;
+    k_cg_check<<<1, 1, 0, cs>>>(st);
+    return launch_check("sb_cg_pap");
+}
+
+int cg_update_impl(int fused, const double *p, const double *ap, double *x, double *r, int64_t n, int64_t bs,
+                   int64_t nb, void *ws, sb_cg_state *st, const LsaArgs *lsa, cudaStream_t cs) {
+    if (!st) {
+        set_error("sb_cg_update: null state");
+        return SB_E_INVALID;
+    }
+    if (fused)  // kernels.py:117-132 with alpha from the state
+        return cg_reduce(2, p, ap, x, r, n, bs, nb, ws, &st->rr_new, &st->active, &st->alpha, cs,
+                         "sb_cg_update", lsa);
+    // cg.py:67-70: x = alpha*p + 1.0*x ; r = (-alpha)*ap + 1.0*r ; rr_new = r.r
+    const DevCoef alpha{&st->alpha, 1.0}, neg_alpha{&st->alpha, -1.0}, one{nullptr, 1.0};
+    if (int rc = cg_axpy(p, x, n, alpha, one, &st->active, cs, "sb_cg_update")) return rc;
+    if (int rc = cg_axpy(ap, r, n, neg_alpha, one, &st->active, cs, "sb_cg_update")) return rc;
+    return cg_reduce(0, r, r, nullptr, nullptr, n, bs, nb, ws, &st->rr_new, &st->active, nullptr, cs,
+                     "sb_cg_update", lsa);
+}
+
 }  // namespace sb
 
 using namespace sb;
@@ -91,34 +121,13 @@ int sb_cg_begin(sb_cg_state *st, const double *rr0, const double *bb, double eps
 int sb_cg_pap(const double *p, const double *ap, int64_t n, int64_t bs, int64_t nb, void *ws, sb_cg_state *st,
               sb_stream_t s) {
     clear_error();
-    if (!st) {
-        set_error("sb_cg_pap: null state");
-        return SB_E_INVALID;
-    }
-    if (int rc = cg_reduce(1, p, ap, nullptr, nullptr, n, bs, nb, ws, &st->pap, &st->active, nullptr,
-                           as_stream(s), "sb_cg_pap"))
-        return rc;
-    k_cg_check<<<1, 1, 0, as_stream(s)>>>(st);
-    return launch_check("sb_cg_pap");
+    return cg_pap_impl(p, ap, n, bs, nb, ws, st, nullptr, as_stream(s));
 }
 
 int sb_cg_update(int fused, const double *p, const double *ap, double *x, double *r, int64_t n, int64_t bs,
                  int64_t nb, void *ws, sb_cg_state *st, sb_stream_t s) {
     clear_error();
-    if (!st) {
-        set_error("sb_cg_update: null state");
-        return SB_E_INVALID;
-    }
-    cudaStream_t cs = as_stream(s);
-    if (fused)  // kernels.py:117-132 with alpha from the state
-        return cg_reduce(2, p, ap, x, r, n, bs, nb, ws, &st->rr_new, &st->active, &st->alpha, cs,
-                         "sb_cg_update");
-    // cg.py:67-70: x = alpha*p + 1.0*x ; r = (-alpha)*ap + 1.0*r ; rr_new = r.r
-    const DevCoef alpha{&st->alpha, 1.0}, neg_alpha{&st->alpha, -1.0}, one{nullptr, 1.0};
-    if (int rc = cg_axpy(p, x, n, alpha, one, &st->active, cs, "sb_cg_update")) return rc;
-    if (int rc = cg_axpy(ap, r, n, neg_alpha, one, &st->active, cs, "sb_cg_update")) return rc;
-    return cg_reduce(0, r, r, nullptr, nullptr, n, bs, nb, ws, &st->rr_new, &st->active, nullptr, cs,
-                     "sb_cg_update");
+    return cg_update_impl(fused, p, ap, x, r, n, bs, nb, ws, st, nullptr, as_stream(s));
 }
 
 int sb_cg_direction(const double *r, double *p, int64_t n, sb_cg_state *st, sb_stream_t s) {

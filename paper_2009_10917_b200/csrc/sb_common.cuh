@@ -54,9 +54,15 @@ __device__ __forceinline__ double coef_value(const DevCoef &c) {
 // when *gate == 0, so a converged solve turns later iterations into no-ops.
 int cg_axpy(const double *x, double *y, int64_t n, DevCoef a, DevCoef b, const int32_t *gate,
             cudaStream_t st, const char *name);
+struct LsaArgs;  // sb_lsa.cuh (multi-GPU combine); nullptr = this rank only
 int cg_reduce(int mode, const double *u, const double *v, double *x, double *r, int64_t n, int64_t bs,
               int64_t nb, void *ws, double *result, const int32_t *gate, const double *alpha,
-              cudaStream_t st, const char *name);
+              cudaStream_t st, const char *name, const LsaArgs *lsa = nullptr);
+// sb_cg.cu bodies shared by the single- and multi-GPU (sb_lsa_cg_*) entry points
+int cg_pap_impl(const double *p, const double *ap, int64_t n, int64_t bs, int64_t nb, void *ws,
+                sb_cg_state *st, const LsaArgs *lsa, cudaStream_t s);
+int cg_update_impl(int fused, const double *p, const double *ap, double *x, double *r, int64_t n, int64_t bs,
+                   int64_t nb, void *ws, sb_cg_state *st, const LsaArgs *lsa, cudaStream_t s);
 
 // Completion ticket of single-launch reductions: a gpu-scope acq_rel add.  The
 // release publishes this CTA's partials (written before the preceding

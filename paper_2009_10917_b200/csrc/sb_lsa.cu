@@ -243,6 +243,22 @@ int sb_lsa_barrier(sb_lsa_t *ctx, sb_stream_t s) {
     return launch_check("sb_lsa_barrier");
 }
 
+int sb_lsa_cg_pap(const double *p, const double *ap, int64_t n, int64_t bs, int64_t nb, void *ws, sb_cg_state *st,
+                  sb_lsa_t *ctx, sb_stream_t s) {
+    clear_error();
+    if (!ctx) { set_error("sb_lsa_cg_pap: null context"); return SB_E_INVALID; }
+    const LsaArgs L = lsa_args(ctx);
+    return cg_pap_impl(p, ap, n, bs, nb, ws, st, &L, as_stream(s));
+}
+
+int sb_lsa_cg_update(int fused, const double *p, const double *ap, double *x, double *r, int64_t n, int64_t bs,
+                     int64_t nb, void *ws, sb_cg_state *st, sb_lsa_t *ctx, sb_stream_t s) {
+    clear_error();
+    if (!ctx) { set_error("sb_lsa_cg_update: null context"); return SB_E_INVALID; }
+    const LsaArgs L = lsa_args(ctx);
+    return cg_update_impl(fused, p, ap, x, r, n, bs, nb, ws, st, &L, as_stream(s));
+}
+
 int sb_lsa_bs3_norm2(const double *x, int64_t n, int64_t bs, int64_t nb, void *ws, double *result, sb_lsa_t *ctx,
                      sb_stream_t s) {
     clear_error();

@@ -561,10 +561,11 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
 
 int cg_reduce(int mode, const double *u, const double *v, double *x, double *r, int64_t n, int64_t bs,
               int64_t nb, void *ws, double *result, const int32_t *gate, const double *alpha,
-              cudaStream_t st, const char *name) {
+              cudaStream_t st, const char *name, const LsaArgs *lsa) {
     RArgs A{};
     A.u = u; A.v = v; A.x = x; A.r = r; A.n = n; A.bs = bs; A.nb = nb; A.result = result;
     A.gate = gate; A.alpha_ptr = alpha;
+    if (lsa) A.lsa = *lsa;
     if (!gate || (n > 0 && (!u || !v || (mode == R_FUSED && (!x || !r || !alpha))))) {
         set_error("%s: invalid arguments", name);
         return SB_E_INVALID;

@@ -139,3 +139,19 @@ def test_bs7_halo_through_lsa_window_bitexact(lsa, K, p, world):
             _lib.check(L.sb_bs7_scatter(ids.data_ptr(), ids.shape[0], win.data_ptr(), win.shape[0],
                                         ql.data_ptr(), 0, st), "scatter")
         assert torch.equal(ql, want[lo:hi]), r
+
+
+@pytest.mark.parametrize("fused,graph", [(True, False), (False, False), (True, True)])
+def test_device_cg_with_fused_combine_one_rank(lsa, fused, graph):
+    """cg_solve_device with the multi-GPU reductions (sb_lsa_cg_*) on a one-rank
+    team reproduces the single-GPU device CG (and so the reference) bit for bit."""
+    from paper_2009_10917_b200 import cg
+    rng = np.random.default_rng(17)
+    d = torch.from_numpy(rng.uniform(1, 50, 20_000)).cuda()
+    b = torch.from_numpy(rng.uniform(-1, 1, 20_000)).cuda()
+    A = cg.diagonal_operator(d)
+    want = cg.cg_solve_device(A, b, torch.zeros_like(b), 1e-20, 300, fused=fused, relative=True)
+    got = cg.cg_solve_device(A, b, torch.zeros_like(b), 1e-20, 300, fused=fused, relative=True,
+                             check_every=8, graph=graph, lsa=lsa)
+    assert got.iterations == want.iterations and got.final_rr == want.final_rr
+    assert torch.equal(got.x, want.x)
