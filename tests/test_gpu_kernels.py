@@ -242,7 +242,7 @@ def test_tma_ring_sizes_and_configs_vs_oracle(sb, oracle, n):
         rng = np.random.default_rng([n, 5])
         xh, yh = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
         x, y = d(xh), d(yh)
-        for bs, nb in ((64, 7), (128, 33), (256, 512), (512, 296), (256, 1184), (256, 3)):
+        for bs, nb in ((64, 7), (128, 33), (256, 512), (512, 296), (256, 1184), (256, 3), (256, 4), (256, 12)):
             cfg = sb.ReductionConfig(bs, nb)
             assert sb.bs3_norm2(x, cfg) == oracle.bs3_norm2(xh, bs, nb), (bs, nb)
             assert sb.bs4_dot(x, y, cfg) == oracle.bs4_dot(xh, yh, bs, nb), (bs, nb)
