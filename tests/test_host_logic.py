@@ -218,6 +218,29 @@ def test_library_exports_every_header_symbol():
     assert L.sb_reduce_workspace_bytes(3, 512) == 0
 
 
+def test_library_argument_validation_without_gpu():
+    """Entry points reject bad arguments with SB_E_INVALID and a message
+    before touching the device (the reference's ValueError cases)."""
+    L = _lib.load_library(_lib.LIB_PATH)
+    E = _lib.SB_E_INVALID
+    assert L.sb_bs1_copy(None, None, -1, None) == E
+    assert b"invalid" in L.sb_last_error()
+    fake = 0x1000  # never dereferenced: the configuration is rejected first
+    assert L.sb_bs3_norm2(fake, 10, 3, 512, fake, fake, None) == E            # block_size not a power of two
+    assert b"power of two" in L.sb_last_error()
+    assert L.sb_bs4_dot(fake, fake, 10, 256, 0, fake, fake, None) == E         # n_blocks < 1
+    assert L.sb_bs6_plan_size(10, 513) == 0 and L.sb_bs6_plan_size(0, 512) == 0
+    assert L.sb_bs6_gather_planned(None, 1, 512, None, None, 10, 10, None, None, None, 0, None) == E
+    assert L.sb_bs7_scatter(None, 5, None, 5, None, 0, None) == E
+    assert L.sb_bs7_scatter_split(None, 5, None, -1, None, 0, None, 0, None) == E
+    assert L.sb_cg_begin(None, None, None, 1e-10, 5, None) == E
+    assert L.sb_cg_pap(None, None, 10, 256, 512, None, None, None) == E
+    assert L.sb_lsa_create(None, 0, 1, 0, None) == E
+    assert L.sb_lsa_bs3_norm2(None, 10, 256, 512, None, None, None, None) == E
+    assert L.sb_lsa_halo_window(None, 8) == E
+    assert L.sb_sum_ordered(None, -1, None, None) == E
+
+
 def test_library_is_sm100a():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
                          capture_output=True, text=True)
