@@ -50,6 +50,7 @@ constexpr int kRingNorm = SB_RING_NORM, kRingDot = SB_RING_DOT, kRingFused = SB_
 #endif
 constexpr int kRingFusedBpc4 = SB_RING_FUSED_BPC4;  // 4 stages of 4 arrays x 8 KB
 
+
 enum RMode { R_NORM = 0, R_DOT = 1, R_FUSED = 2 };
 
 struct RArgs {
