@@ -1,0 +1,68 @@
+"""Parity at BASELINE.json's full sizes on one B200 (180 GB):
+
+* config 4's BS5 (and BS3/BS4) at n = 1e9 DOFs: the scalars bitwise against
+  the lattice oracle run on all host cores, the updated x, r bitwise against
+  its in-place results;
+* config 5's mesh (K=143, N=7: NL = 1.497e9, NG = 1.006e9 -- the global
+  problem the 8-GPU run partitions) gathered and scattered whole on one GPU,
+  checked through exact size-independent identities: BS7 equals plain
+  indexing q_global[l2g], and Z^T Z x == multiplicity * x with integer-valued
+  x (|sum| < 2^53, so the ordered fp64 row sums are exact).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import paper_2009_10917_b200 as sb
+    from paper_2009_10917_b200 import _lib
+    _lib.lib()
+    return sb
+
+
+def test_c4_reductions_at_1e9_vs_oracle(sb, oracle):
+    n = 1_000_000_000
+    gen = torch.Generator(device="cuda"); gen.manual_seed(2009)
+    x = torch.empty(n, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
+    y = torch.empty(n, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
+    xh, yh = x.cpu().numpy(), y.cpu().numpy()
+    oracle.set_threads(oracle.max_threads())
+    try:
+        cfg = sb.ReductionConfig()
+        assert sb.bs3_norm2(x, cfg) == oracle.bs3_norm2(xh)
+        assert sb.bs4_dot(x, y, cfg) == oracle.bs4_dot(xh, yh)
+        # BS5 with p = y, ap = x updating copies of (x, y)
+        want = oracle.bs5_fused_cg_update(0.375, yh, xh, xh.copy(), yh.copy())
+        xx, rr = x.clone(), y.clone()
+        got = sb.bs5_fused_cg_update(0.375, y, x, xx, rr)
+        assert got == want
+        xo, ro = xh.copy(), yh.copy()
+        oracle.bs5_fused_cg_update(0.375, yh, xh, xo, ro)
+        assert np.array_equal(xx.cpu().numpy(), xo) and np.array_equal(rr.cpu().numpy(), ro)
+    finally:
+        oracle.set_threads(1)
+
+
+def test_c5_mesh_gather_scatter_whole_on_one_gpu(sb):
+    K, p = 143, 7
+    mesh = sb.build_mesh(K, p)
+    assert (mesh.nl, mesh.ng) == (1_497_193_984, 1_006_012_008)
+    ids = sb.build_scatter_ids(mesh)
+    gen = torch.Generator(device="cuda"); gen.manual_seed(5)
+    xg = torch.randint(-(1 << 20), 1 << 20, (mesh.ng,), generator=gen, device="cuda").to(torch.float64)
+    ql = torch.empty(mesh.nl, dtype=torch.float64, device="cuda")
+    sb.bs7_scatter(ids, xg, ql)
+    l2g = mesh.local_to_global
+    step = 100_000_000
+    for a in range(0, mesh.nl, step):  # BS7 == plain indexing, chunk by chunk
+        assert torch.equal(ql[a:a + step], xg[l2g[a:a + step].long()])
+    op = sb.build_gather(mesh)
+    del ids
+    out = sb.bs6_gather(op, ql)
+    mult = sb.multiplicity(mesh)
+    assert torch.equal(out, mult * xg)  # Z^T Z x = diag(Z^T 1) x, exact for integer x
