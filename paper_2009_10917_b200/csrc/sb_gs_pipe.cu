@@ -12,11 +12,13 @@
 // the 8-byte gathers; so was a two-deep variant that overlapped one
 // super-block's row sums with the next one's gathers.)
 //
-// BS6 is L1-throughput bound, not DRAM bound (ncu at N=7: l1tex 78% busy,
-// DRAM 66%): every gather instruction costs one L1 tag lookup per distinct
-// 128 B line its lanes touch, and the one-thread-per-row sums cost shared
-// memory wavefronts.  The kernels below are shaped to cut both (see
-// scripts/expt/bs6_diag.cu and profiles/r01_bs6_variants.md).
+// BS6 is bounded by the L1 data pipe as much as by DRAM (ncu at N=7, product
+// kernel: l1tex wavefronts 79% of peak, DRAM 76%; the r01 kernel was at 78% /
+// 66%): every gather instruction costs one L1 tag lookup per distinct 128 B
+// line its lanes touch, and the one-thread-per-row sums cost shared-memory
+// wavefronts.  The kernels below are shaped to cut both; ~20 variants that
+// did not (TMA-fed, two-deep, row-mapped, partner plans, TMA gather4, ...)
+// are recorded in profiles/r01_bs6_variants.md.
 //
 // Results are bitwise those of the one-tile kernels: BS6 still sums each row
 // in ascending column order from +0.0 (or the carry-in) in one thread.
