@@ -162,7 +162,8 @@ def cpu_model():
 
 # ------------------------------------------------------------ CPU (oracle)
 
-def run_cpu_sample(seconds: float, K: int, order: int, bs: int, nb: int, port: str = "numpy"):
+def run_cpu_sample(seconds: float, K: int, order: int, bs: int, nb: int, port: str = "numpy",
+                   threads: int | None = None, n: int | None = None, Kc: int | None = None):
     """Time a CPU port of the reference hot path on all host threads over a
     bounded sample of the workload (BS1-BS5 at n_cpu, BS6/BS7 at K_cpu):
       port="numpy": oracle/np_port.py -- the reference's own implementation
@@ -173,10 +174,10 @@ def run_cpu_sample(seconds: float, K: int, order: int, bs: int, nb: int, port: s
     from oracle import oracle as O
     from paper_2009_10917_b200.core import bytes_moved
 
-    threads = cpu_cores()
+    threads = threads or cpu_cores()
     O.set_threads(threads)
-    n = 20_000_000 if port == "c" else 10_000_000
-    Kc = max(2, min(K, 33 if port == "c" else 24))
+    n = n or (20_000_000 if port == "c" else 10_000_000)
+    Kc = Kc or max(2, min(K, 33 if port == "c" else 24))
     rng = np.random.default_rng([0, n])
     x, y, p, ap = (rng.uniform(-1, 1, n) for _ in range(4))
     l2g = O.build_mesh(Kc, order)
@@ -533,6 +534,7 @@ def main_ours(args):
                        **({"collective": dist_ctx.collective} if dist_ctx is not None else {}),
                        "l2": "every input > L2 (126 MB); no flush between steps"},
             "frac_of_peak": round(value / agg_peak, 4),
+            "frac_of_nominal_8TBps": round(value / (8000.0 * world), 4),
             "per_test": per_test, "roofline": roof,
             "gpu_launches": w.launches_per_step * args.steps,
             "clocks": clk.summary(),
@@ -547,9 +549,14 @@ def main_ours(args):
                                                    args.block_size, args.n_blocks, "numpy")
             vc, _, sample_c, per_c = run_cpu_sample(args.cpu_seconds / 2, args.K, args.order,
                                                     args.block_size, args.n_blocks, "c")
+            # BASELINE config 1 (C1: K=16, N=7; BS1-BS5 at n = NG = 1,442,897), one thread
+            v1, _, sample_1, per_1 = run_cpu_sample(min(5.0, args.cpu_seconds / 3), 16, 7, args.block_size,
+                                                    args.n_blocks, "numpy", threads=1, n=1_442_897, Kc=16)
             result["cpu_baseline"] = {
                 "value": round(v, 3), "unit": "GB/s", "cores": cores, "kind": "port",
                 "sample": sample, "per_test": {k: round(x, 3) for k, x in per.items()},
+                "c1_single_thread": {"value": round(v1, 3), "cores": 1, "sample": sample_1,
+                                     "per_test": {k: round(x, 3) for k, x in per_1.items()}},
                 "c_port": {"value": round(vc, 3), "sample": sample_c,
                            "per_test": {k: round(x, 3) for k, x in per_c.items()},
                            "note": "same algorithm restated in C + OpenMP (stronger than "
