@@ -54,6 +54,24 @@ def _all_cuda(*vs) -> bool:
     return all(isinstance(v, torch.Tensor) and v.is_cuda for v in vs)
 
 
+_F64 = torch.float64
+
+
+def _fast_vecs(*vs):
+    """Device of the arguments when they are all contiguous 1-D float64 CUDA
+    tensors of one length on one device (the hot path), else None -- the
+    caller then runs the full checks, which raise the reference's errors."""
+    v0 = vs[0]
+    if type(v0) is not torch.Tensor or not v0.is_cuda:
+        return None
+    dev, n = v0.device, v0.shape
+    for v in vs:
+        if (type(v) is not torch.Tensor or v.dtype is not _F64 or v.shape != n or len(n) != 1
+                or not v.is_cuda or v.device != dev or not v.is_contiguous()):
+            return None
+    return dev
+
+
 def _stage_all(names, vs):
     dev = None
     for v in vs:
@@ -83,7 +101,7 @@ def _same_device(*vs) -> torch.device:
 def _result(dev, out):
     if out is None:
         return torch.empty(1, dtype=torch.float64, device=dev)
-    if not (out.is_cuda and out.dtype == torch.float64 and out.numel() >= 1 and out.device == dev):
+    if not (out.is_cuda and out.dtype is _F64 and out.numel() >= 1 and out.device == dev):
         raise ValueError("out must be a float64 device tensor on the inputs' device")
     return out
 
@@ -92,6 +110,11 @@ def _result(dev, out):
 
 def bs1_copy(x, y) -> None:
     """kernels.py:90-93: y = x (in place)."""
+    dev = _fast_vecs(x, y)
+    if dev is not None:
+        _lib.check(_lib.lib().sb_bs1_copy(x.data_ptr(), y.data_ptr(), x.shape[0], _lib.stream_handle(dev)),
+                   "bs1_copy")
+        return
     check_same_length(x, y)
     if _all_cuda(x, y):
         _check_vec(x, "x"); _check_vec(y, "y")
@@ -114,6 +137,11 @@ def bs1_copy(x, y) -> None:
 
 def bs2_axpy(alpha: float, x, beta: float, y) -> None:
     """kernels.py:96-103: y = alpha*x + beta*y, one rounded multiply-add pair per element."""
+    dev = _fast_vecs(x, y)
+    if dev is not None:
+        _lib.check(_lib.lib().sb_bs2_axpy(float(alpha), x.data_ptr(), float(beta), y.data_ptr(), x.shape[0],
+                                          _lib.stream_handle(dev)), "bs2_axpy")
+        return
     check_same_length(x, y)
     if _all_cuda(x, y):
         _check_vec(x, "x"); _check_vec(y, "y")
@@ -147,8 +175,10 @@ def _cfg(cfg: ReductionConfig) -> ReductionConfig:
 def bs3_norm2_async(x: DVector, cfg: ReductionConfig = DEFAULT_REDUCTION, out=None) -> torch.Tensor:
     """bs3_norm2 leaving the scalar on the device (no host sync)."""
     cfg = _cfg(cfg)
-    _check_vec(x, "x")
-    dev = x.device
+    dev = _fast_vecs(x)
+    if dev is None:
+        _check_vec(x, "x")
+        dev = x.device
     L = _lib.lib()
     st = _lib.stream_handle(dev)
     ws = _lib.workspace(dev, st, cfg.block_size, cfg.n_blocks)
@@ -170,9 +200,11 @@ def bs3_norm2(x, cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
 def bs4_dot_async(x: DVector, y: DVector, cfg: ReductionConfig = DEFAULT_REDUCTION,
                   out=None) -> torch.Tensor:
     cfg = _cfg(cfg)
-    check_same_length(x, y)
-    _check_vec(x, "x"); _check_vec(y, "y")
-    dev = _same_device(x, y)
+    dev = _fast_vecs(x, y)
+    if dev is None:
+        check_same_length(x, y)
+        _check_vec(x, "x"); _check_vec(y, "y")
+        dev = _same_device(x, y)
     L = _lib.lib()
     st = _lib.stream_handle(dev)
     ws = _lib.workspace(dev, st, cfg.block_size, cfg.n_blocks)
@@ -198,10 +230,12 @@ def bs4_dot(x, y, cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
 def bs5_fused_cg_update_async(alpha: float, p: DVector, ap: DVector, x: DVector, r: DVector,
                               cfg: ReductionConfig = DEFAULT_REDUCTION, out=None) -> torch.Tensor:
     cfg = _cfg(cfg)
-    check_same_length(p, ap, x, r)
-    for v, nm in ((p, "p"), (ap, "ap"), (x, "x"), (r, "r")):
-        _check_vec(v, nm)
-    dev = _same_device(p, ap, x, r)
+    dev = _fast_vecs(p, ap, x, r)
+    if dev is None:
+        check_same_length(p, ap, x, r)
+        for v, nm in ((p, "p"), (ap, "ap"), (x, "x"), (r, "r")):
+            _check_vec(v, nm)
+        dev = _same_device(p, ap, x, r)
     L = _lib.lib()
     st = _lib.stream_handle(dev)
     ws = _lib.workspace(dev, st, cfg.block_size, cfg.n_blocks)
