@@ -121,7 +121,7 @@ def lib() -> ctypes.CDLL:
                 if not torch.cuda.is_available():
                     raise SB200Unavailable("no CUDA device visible: the sb200 kernels need a B200 "
                                            "(sm_100a); there is no CPU fallback")
-                _lib = load_library()
+                _lib = load_library(os.environ.get("SB200_LIB", LIB_PATH))  # (A/B builds)
     return _lib
 
 

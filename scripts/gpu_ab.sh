@@ -1,6 +1,7 @@
 set -x
-rm -f gpurun_out/bs6_deep.log
-SB200_BS6_CFG=deep,0,8 timeout 600 python -m pytest tests/test_gpu_gs.py -q -x -p no:cacheprovider 2>&1 | tail -2 >> gpurun_out/bs6_deep.log
-timeout 300 python scripts/expt/time_bs6.py 2 3 5 7 15 >> gpurun_out/bs6_deep.log 2>&1
-for c in deep,0,8 deep,0,10 deep,0,6 deep,1,8; do SB200_BS6_CFG=$c timeout 300 python scripts/expt/time_bs6.py 2 3 5 7 15 >> gpurun_out/bs6_deep.log 2>&1; done
-cat gpurun_out/bs6_deep.log
+timeout 300 python scripts/expt/time_bs6.py 1 2 3 5 7 15 > gpurun_out/bs6_keep.log 2>&1
+SB200_LIB=scripts/expt/_alt/libsb200.so timeout 300 python scripts/expt/time_bs6.py 1 2 3 5 7 15 >> gpurun_out/bs6_keep.log 2>&1
+for L in paper_2009_10917_b200/lib/libsb200.so scripts/expt/_alt/libsb200.so; do
+SB200_LIB=$L timeout 300 ncu --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:k_bs6 -s 2 -c 1 python scripts/expt/time_bs6.py 1 2>&1 | grep -E "dram__|gpu__time" >> gpurun_out/bs6_keep.log
+done
+cat gpurun_out/bs6_keep.log
