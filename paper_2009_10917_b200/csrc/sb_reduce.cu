@@ -174,7 +174,9 @@ __device__ __forceinline__ void second_stage(const RArgs &A, double *sm, int bs,
     for (int j = 0; j < spt; j++) {
         const int t = threadIdx.x + j * T;
         double acc = 0.0;
-        for (int64_t c = t; c < A.nb; c += bs) acc = add(acc, __ldcg(A.partials + c));
+        // only the launched blocks have partials (see launch_reduce: blocks
+        // past n hold +0.0, and acc + 0.0 == acc for an acc that started at +0.0)
+        for (int64_t c = t; c < (int64_t)gridDim.x; c += bs) acc = add(acc, __ldcg(A.partials + c));
         sm[t] = acc;
     }
     __syncthreads();
@@ -533,7 +535,13 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
 #undef SB_TMA
         return launch_check(name);
     }
-#define SB_LAT(T_, SPT_) k_lattice<T_, SPT_, MODE, U><<<grid, T_, 0, st>>>(A)
+    // For n < S every lattice block past ceil(n / bs) is empty: its slots
+    // stay +0.0, its tree gives +0.0, and adding +0.0 in the final reduce
+    // leaves any running sum (which starts at +0.0 and so is never -0.0)
+    // unchanged -- launching only the non-empty blocks is bitwise the same
+    // and cuts the small-n fixed cost (fewer CTAs on the completion ticket).
+    const unsigned grid_lat = A.n < A.S ? (unsigned)std::max<int64_t>(1, (A.n + A.bs - 1) / A.bs) : grid;
+#define SB_LAT(T_, SPT_) k_lattice<T_, SPT_, MODE, U><<<grid_lat, T_, 0, st>>>(A)
     switch (A.bs) {
         case 2: SB_LAT(2, 1); break;
         case 4: SB_LAT(4, 1); break;
