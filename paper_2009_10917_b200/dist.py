@@ -305,23 +305,60 @@ class DistScatter:
         self.down_ptrs = ([lsa.halo_pointers(offset + e * nb, self.rank - 1)[1] for e in (0, 1)]
                           if self.rank > 0 else None)
 
-    def scatter_lsa(self, q_local: torch.Tensor) -> None:
+    def scatter_lsa(self, q_local: torch.Tensor, own: torch.Tensor | None = None) -> None:
+        """BS7 over the slab with the NVLink halo; `own` (default: the window's
+        own rows) holds this rank's q_global rows."""
         L = _lib.lib()
         e = self.epoch
         self.epoch ^= 1
         st = _lib.stream_handle(self.device)
         plane = self.part.plane
+        src = self.window if own is None else own
         if self.down_ptrs is not None:  # my bottom plane -> rank-1's halo buffer, over NVLink
-            _lib.check(L.sb_bs1_copy(self.window.data_ptr(), self.down_ptrs[e], plane, st), "bs7 halo put")
+            _lib.check(L.sb_bs1_copy(src.data_ptr(), self.down_ptrs[e], plane, st), "bs7 halo put")
         self.lsa.barrier()
         nl = int(self.ids.shape[0])
         if self.halo_ptrs is None:  # last rank owns its top plane
-            _lib.check(L.sb_bs7_scatter(self.ids.data_ptr(), nl, self.window.data_ptr(),
-                                        int(self.window.shape[0]), q_local.data_ptr(), 0, st), "bs7_scatter")
+            n_own = int(src.shape[0]) if own is not None else int(self.window.shape[0])
+            _lib.check(L.sb_bs7_scatter(self.ids.data_ptr(), nl, src.data_ptr(), n_own, q_local.data_ptr(), 0, st),
+                       "bs7_scatter")
         else:
-            _lib.check(L.sb_bs7_scatter_split(self.ids.data_ptr(), nl, self.window.data_ptr(), self.own_rows,
+            _lib.check(L.sb_bs7_scatter_split(self.ids.data_ptr(), nl, src.data_ptr(), self.own_rows,
                                               self.halo_ptrs[e], plane, q_local.data_ptr(), 0, st),
                        "bs7_scatter_split")
+
+
+class DistMassOperator:
+    """A = Z^T diag(w) Z on the rank's rows of a z-slab partitioned mesh -- the
+    distributed form of cg.gather_scatter_operator, for
+    cg.cg_solve_device(..., lsa=...): BS7 with the NVLink halo (split scatter),
+    the pointwise weight, BS6 with the NVLink carry.  Every step is stream
+    ordered on this rank (LSA barriers synchronise with the neighbours), so a
+    CG iteration never waits on the host.  `weights` are this rank's
+    element-local values (length part.nl(rank)); apply() maps the rank's
+    owned rows (part.ng_own(rank)) to the same rows of A p."""
+
+    def __init__(self, part: SlabPartition, rank: int, device, weights, lsa):
+        self.part, self.rank, self.device = part, rank, torch.device(device)
+        self.scat = DistScatter.build(part, rank, device)
+        self.gath = DistGather.build(part, rank, device)
+        nb = 8 * part.plane
+        lsa.halo_window(4 * nb)  # [BS6 carry x2 | BS7 halo x2]
+        self.gath.enable_lsa(lsa, 0)
+        self.scat.enable_lsa(lsa, 2 * nb)
+        self.w = torch.as_tensor(weights, dtype=torch.float64).to(self.device)
+        if self.w.shape[0] != part.nl(rank):
+            raise ValueError("weights must have one entry per element-local node of this rank's slab")
+        self.ql = torch.empty(part.nl(rank), dtype=torch.float64, device=self.device)
+        self.n_own = part.ng_own(rank)
+
+    def __call__(self, p_own: torch.Tensor) -> torch.Tensor:
+        if p_own.shape[0] != self.n_own:
+            raise ValueError(f"expected this rank's {self.n_own} rows, got {p_own.shape[0]}")
+        self.scat.scatter_lsa(self.ql, own=p_own)
+        self.ql.mul_(self.w)
+        out = torch.empty(self.n_own, dtype=torch.float64, device=self.device)
+        return self.gath.gather_lsa(self.ql, out)
 
 
 def _gpu_scatter(ids: torch.Tensor, window: torch.Tensor, q_local: torch.Tensor) -> None:

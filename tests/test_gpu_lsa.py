@@ -155,3 +155,31 @@ def test_device_cg_with_fused_combine_one_rank(lsa, fused, graph):
                              check_every=8, graph=graph, lsa=lsa)
     assert got.iterations == want.iterations and got.final_rr == want.final_rr
     assert torch.equal(got.x, want.x)
+
+
+def test_dist_mass_operator_and_cg_one_rank(lsa):
+    """dist.DistMassOperator (BS7 + NVLink halo, weight, BS6 + NVLink carry) on a
+    one-rank partition equals cg.gather_scatter_operator, and the fully
+    device-resident CG through it (lsa-combined scalars) equals the
+    single-GPU device CG bit for bit."""
+    import paper_2009_10917_b200 as sb
+    from paper_2009_10917_b200 import cg
+    from paper_2009_10917_b200 import dist as D
+    from paper_2009_10917_b200 import lsa as LSA
+    K, p = 5, 3
+    mesh = sb.build_mesh(K, p)
+    rng = np.random.default_rng(21)
+    w = rng.uniform(1, 2, mesh.nl)
+    A1 = cg.gather_scatter_operator(sb.build_gather(mesh), sb.build_scatter_ids(mesh), w)
+    # a fresh context: the halo window is allocated once per context
+    ctx = LSA.LsaReducer(1, 0, "cuda:0", unique_id=LSA.LsaReducer.unique_id())
+    try:
+        Ad = D.DistMassOperator(D.SlabPartition(K, p, 1), 0, "cuda:0", w, ctx)
+        x = torch.from_numpy(rng.uniform(-1, 1, mesh.ng)).cuda()
+        assert torch.equal(Ad(x), A1(x))
+        b = torch.from_numpy(rng.uniform(-1, 1, mesh.ng)).cuda()
+        want = cg.cg_solve_device(A1, b, torch.zeros_like(b), 1e-22, 500, relative=True)
+        got = cg.cg_solve_device(Ad, b, torch.zeros_like(b), 1e-22, 500, relative=True, lsa=ctx, check_every=8)
+        assert got.iterations == want.iterations and torch.equal(got.x, want.x)
+    finally:
+        ctx.close()
