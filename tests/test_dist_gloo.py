@@ -137,3 +137,39 @@ def test_slab_partition_arithmetic():
         D.SlabPartition(3, 2, 4)
     assert [D.rank_span(10, 4, r) for r in range(4)] == [(0, 3), (3, 6), (6, 8), (8, 10)]
     assert D.rank_span(2, 4, 3) == (2, 2)
+
+
+def _agree_worker(rank, world, port, fail_rank, results):
+    """BenchContext's fused-path agreement: if the NVLink context cannot be set
+    up on one rank, every rank must fall back (the fused kernels are
+    collective, a split decision would hang)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2009_10917_b200 import lsa as LSA
+        closed = []
+
+        class FakeLsa:
+            def __init__(self, w, r, device, group=None, unique_id=None):
+                if r == fail_rank:
+                    raise LSA.LsaUnavailable("simulated: not an NVLink peer")
+
+            def close(self):
+                closed.append(True)
+
+        LSA.LsaReducer = FakeLsa
+        ctx = D.BenchContext(rank, world, types.SimpleNamespace(K=4, order=2), "cpu", use_lsa=True)
+        results[rank] = (ctx.lsa is None, "unavailable" in ctx.collective, bool(closed) or rank == fail_rank)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [0, 1])
+def test_fused_path_agreement_falls_back_on_every_rank(fail_rank):
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_agree_worker, args=(world, _free_port(), fail_rank, results), nprocs=world, join=True)
+    for r in range(world):
+        assert results[r] == (True, True, True), (r, results[r])
