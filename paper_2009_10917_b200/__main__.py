@@ -1,5 +1,6 @@
-import sys
+"""`python -m paper_2009_10917_b200 ...` runs the CLI (cli.main)."""
 
-from .cli import main
+if __name__ == "__main__":
+    from .cli import main
 
-sys.exit(main())
+    raise SystemExit(main())

@@ -32,16 +32,12 @@ def max_workers() -> int:
 
 
 def split_range(n: int, parts: int) -> list[tuple[int, int]]:
-    """parallel.py:43-53: at most `parts` contiguous non-empty spans of range(n).
+    """Contiguous (lo, hi) spans covering range(n), at most `parts` of them,
+    lengths differing by at most one, longer spans first (parallel.py:43-53).
 
     Used by the multi-GPU partitioner (dist.py) to cut vectors into rank chunks.
     """
-    parts = max(1, min(parts, n))
-    step, extra = divmod(n, parts)
-    spans = []
-    lo = 0
-    for i in range(parts):
-        hi = lo + step + (1 if i < extra else 0)
-        spans.append((lo, hi))
-        lo = hi
-    return spans
+    k = max(1, min(parts, n))
+    base, longer = divmod(n, k)
+    edge = [i * base + min(i, longer) for i in range(k + 1)]
+    return list(zip(edge[:-1], edge[1:]))
