@@ -106,6 +106,7 @@ struct Step<R_NORM> {
     double a;
     __device__ __forceinline__ void load(const RArgs &A, int64_t i) { a = ld_stream(A.u + i); }
     __device__ __forceinline__ double term(const RArgs &) const { return mul(a, a); }
+    __device__ __forceinline__ void pin() { asm volatile("" : "+d"(a)); }
 };
 template <>
 struct Step<R_DOT> {
@@ -115,6 +116,7 @@ struct Step<R_DOT> {
         b = ld_stream(A.v + i);
     }
     __device__ __forceinline__ double term(const RArgs &) const { return mul(a, b); }
+    __device__ __forceinline__ void pin() { asm volatile("" : "+d"(a), "+d"(b)); }
 };
 template <>
 struct Step<R_FUSED> {
@@ -125,6 +127,7 @@ struct Step<R_FUSED> {
         x = ld_stream(A.x + i);
         r = ld_stream(A.r + i);
     }
+    __device__ __forceinline__ void pin() { asm volatile("" : "+d"(p), "+d"(ap), "+d"(x), "+d"(r)); }
     // x += alpha*p ; r -= alpha*ap (kernels.py:127-131); returns r_new^2
     __device__ __forceinline__ double update_store(const RArgs &A, int64_t i) {
         const double xn = add(x, mul(A.alpha, p));
@@ -187,6 +190,43 @@ __device__ __forceinline__ void second_stage(const RArgs &A, double *sm, int bs,
     }
 }
 
+// The last, partial batch of a chain (fewer than U steps left): all of its
+// loads first, then the in-order adds (and BS5's stores), so a ragged chain
+// costs one memory latency instead of one per remaining step.  The batch
+// ends with a branch at the first step past n rather than predicating every
+// load: U*SPT live predicates would not fit the 7 predicate registers (the
+// compiler then splits the batch), and clamped re-loads of a valid element
+// hot-spot one L2 slice when every thread's chain is short (n < S).
+template <int T, int SPT, int MODE, int U>
+__device__ __forceinline__ void ragged_batch(const RArgs &A, int64_t c0, double (&acc)[SPT]) {
+    const int64_t S = A.S, n = A.n;
+    Step<MODE> st[U][SPT];
+#pragma unroll
+    for (int k = 0; k < U; k++) {
+        const int64_t ik = c0 + (int64_t)k * S;
+        if (ik >= n) break;
+#pragma unroll
+        for (int j = 0; j < SPT; j++)
+            if (ik + (int64_t)j * T < n) st[k][j].load(A, ik + (int64_t)j * T);
+    }
+    // keep the compiler from hoisting step 0's arithmetic between the loads
+    // of the later steps (it knows step 0 exists; BS5 otherwise loses a latency)
+#pragma unroll
+    for (int k = 0; k < U; k++)
+#pragma unroll
+        for (int j = 0; j < SPT; j++) st[k][j].pin();
+#pragma unroll
+    for (int k = 0; k < U; k++) {
+        const int64_t ik = c0 + (int64_t)k * S;
+        if (ik >= n) break;
+#pragma unroll
+        for (int j = 0; j < SPT; j++) {
+            const int64_t i = ik + (int64_t)j * T;
+            if (i < n) acc[j] = add(acc[j], step_term<MODE>(st[k][j], A, i));
+        }
+    }
+}
+
 template <int T, int SPT, int MODE, int U>
 __global__ void __launch_bounds__(T, (1024 / T) < 32 ? (1024 / T) : 32) k_lattice(RArgs Ain) {
     RArgs A = Ain;
@@ -214,18 +254,10 @@ __global__ void __launch_bounds__(T, (1024 / T) < 32 ? (1024 / T) : 32) k_lattic
             for (int j = 0; j < SPT; j++)
                 acc[j] = add(acc[j], step_term<MODE>(st[k][j], A, c0 + (int64_t)k * S + (int64_t)j * T));
     }
-    // remainder steps, guarded, still in chain order
-    for (; c0 < n; c0 += S) {
-#pragma unroll
-        for (int j = 0; j < SPT; j++) {
-            const int64_t i = c0 + (int64_t)j * T;
-            if (i < n) {
-                Step<MODE> st;
-                st.load(A, i);
-                acc[j] = add(acc[j], step_term<MODE>(st, A, i));
-            }
-        }
-    }
+    // fewer than U steps are left (c0 + U*S > n, as S > (SPT-1)*T): one more
+    // batch, in its own (non-inlined) function so it does not perturb the
+    // register allocation and load-then-add schedule of the loop above
+    if (c0 < n) ragged_batch<T, SPT, MODE, U>(A, c0, acc);
 #pragma unroll
     for (int j = 0; j < SPT; j++) sm[threadIdx.x + j * T] = acc[j];
     __syncthreads();
@@ -462,6 +494,16 @@ static bool use_tma() {
     return on;
 }
 
+// SB200_TMA_MIN=<n> moves every mode's register/TMA crossover to n elements
+// (tests drive the TMA ring at ragged sizes below the default crossovers).
+static int64_t tma_min_override() {
+    static const int64_t v = [] {
+        const char *e = getenv("SB200_TMA_MIN");
+        return e && e[0] ? (int64_t)atoll(e) : (int64_t)-1;
+    }();
+    return v;
+}
+
 template <int MODE>
 static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
     clear_error();
@@ -486,13 +528,20 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
     // TMA ring: ~32 KB of stages per CTA (so <= 4 CTAs/SM by shared memory)
     constexpr int NA = NArr<MODE>::v;
     const bool tma_ok = aligned16(A.u) && aligned16(A.v) && (MODE != R_FUSED || (aligned16(A.x) && aligned16(A.r)));
-    // Below a few MB per array the register-pipelined lattice has the lower
-    // fixed cost (graph-timed T0 5.7 vs 6.2 us for BS3, 4.9 vs 6.3 for BS4, 6.5
-    // vs 7.5 for BS5) and wins while the data is L2-resident; from ~1e7 DOFs
-    // the TMA ring streams faster (profiles/r01_model_fit.md).  Same lattice,
-    // bitwise the same scalar either way.
-    constexpr int64_t kTmaMinN = MODE == R_FUSED ? 3000000 : 6000000;
-    if (tma_ok && use_tma() && A.n >= kTmaMinN && (A.bs == 64 || A.bs == 128 || A.bs == 256 || A.bs == 512)) {
+    // Register-pipelined lattice below these sizes, TMA ring above: measured
+    // crossovers with L2 flushed before every timed batch (graph timer,
+    // scripts/expt/run_lat_small.py, profiles/r01_lattice_latency.md) -- BS3
+    // ~48M, BS4 ~16M, BS5 ~3M elements.  Same lattice, bitwise the same
+    // scalar either way.
+#ifndef SB_TMA_MIN_FUSED
+#define SB_TMA_MIN_FUSED 3000000
+#define SB_TMA_MIN_DOT 16000000
+#define SB_TMA_MIN_NORM 48000000
+#endif
+    constexpr int64_t kTmaMinN =
+        MODE == R_FUSED ? SB_TMA_MIN_FUSED : (MODE == R_DOT ? SB_TMA_MIN_DOT : SB_TMA_MIN_NORM);
+    const int64_t tma_min = tma_min_override() >= 0 ? tma_min_override() : kTmaMinN;
+    if (tma_ok && use_tma() && A.n >= tma_min && (A.bs == 64 || A.bs == 128 || A.bs == 256 || A.bs == 512)) {
         // ring shape (stages x steps per stage): ~32-48 KB of stages per CTA
         constexpr int SPS = MODE == R_NORM ? kSpsNorm : (MODE == R_DOT ? kSpsDot : kSpsFused);
         constexpr int RING = MODE == R_NORM ? kRingNorm : (MODE == R_DOT ? kRingDot : kRingFused);

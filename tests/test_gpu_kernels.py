@@ -232,27 +232,47 @@ def test_large_n_bitwise_vs_oracle(sb, oracle, n):
         oracle.set_threads(1)
 
 
+_TMA_RING_CHECK = r'''
+import sys
+import numpy as np, torch
+sys.path.insert(0, ".")
+import paper_2009_10917_b200 as sb
+from oracle import oracle
+n = int(sys.argv[1])
+oracle.set_threads(oracle.max_threads())
+rng = np.random.default_rng([n, 5])
+xh, yh = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+x, y = (torch.from_numpy(a).cuda() for a in (xh, yh))
+for bs, nb in ((64, 7), (128, 33), (256, 512), (512, 296), (256, 1184), (256, 3), (256, 4), (256, 12)):
+    cfg = sb.ReductionConfig(bs, nb)
+    assert sb.bs3_norm2(x, cfg) == oracle.bs3_norm2(xh, bs, nb), ("bs3", bs, nb)
+    assert sb.bs4_dot(x, y, cfg) == oracle.bs4_dot(xh, yh, bs, nb), ("bs4", bs, nb)
+    xo, ro = xh.copy(), yh.copy()
+    want = oracle.bs5_fused_cg_update(0.375, yh, xh, xo, ro, bs, nb)
+    xx, rr = x.clone(), y.clone()
+    assert sb.bs5_fused_cg_update(0.375, y, x, xx, rr, cfg) == want, ("bs5", bs, nb)
+    assert np.array_equal(xx.cpu().numpy(), xo) and np.array_equal(rr.cpu().numpy(), ro)
+print("ok")
+'''
+
+
+@pytest.mark.parametrize("tma_min", ["", "0"])
 @pytest.mark.parametrize("n", [6_000_000, 6_000_001, 7_340_033, 12_582_917])
-def test_tma_ring_sizes_and_configs_vs_oracle(sb, oracle, n):
-    """The TMA-ring lattice (taken from 3-6 M elements on) at ragged sizes:
-    leftover chain steps that do not fill a stage, a partial last chunk, and
-    block sizes 64..512 -- bitwise the lattice oracle."""
-    oracle.set_threads(oracle.max_threads())
-    try:
-        rng = np.random.default_rng([n, 5])
-        xh, yh = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
-        x, y = d(xh), d(yh)
-        for bs, nb in ((64, 7), (128, 33), (256, 512), (512, 296), (256, 1184), (256, 3), (256, 4), (256, 12)):
-            cfg = sb.ReductionConfig(bs, nb)
-            assert sb.bs3_norm2(x, cfg) == oracle.bs3_norm2(xh, bs, nb), (bs, nb)
-            assert sb.bs4_dot(x, y, cfg) == oracle.bs4_dot(xh, yh, bs, nb), (bs, nb)
-            xo, ro = xh.copy(), yh.copy()
-            want = oracle.bs5_fused_cg_update(0.375, yh, xh, xo, ro, bs, nb)
-            xx, rr = x.clone(), y.clone()
-            assert sb.bs5_fused_cg_update(0.375, y, x, xx, rr, cfg) == want, (bs, nb)
-            assert np.array_equal(h(xx), xo) and np.array_equal(h(rr), ro)
-    finally:
-        oracle.set_threads(1)
+def test_tma_ring_sizes_and_configs_vs_oracle(n, tma_min):
+    """Both lattice kernels at ragged sizes, bitwise the lattice oracle: the
+    default crossovers (register lattice for BS3/BS4 here, its ragged last
+    batch included; TMA ring for BS5) and, with SB200_TMA_MIN=0, the TMA ring
+    for every mode -- leftover chain steps that do not fill a stage, a partial
+    last chunk, block sizes 64..512.  Run in a subprocess (the override is
+    read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SB200_TMA_MIN=tma_min)
+    r = subprocess.run([sys.executable, "-c", _TMA_RING_CHECK, str(n)], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr[-2000:]
 
 
 def test_fallback_kernels_match(sb):
