@@ -23,6 +23,8 @@
 
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "sb_common.cuh"
 #include "sb_lsa.cuh"
 
@@ -435,6 +437,106 @@ __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs Ain) {
 }
 
 // ---- generic path (block_size > 1024): lattice in global memory ----------
+// The reference tree over 256 slots held by one warp, lane l owning slots
+// l + 32j in v[j]: levels 128, 64, 32 are register adds, 16..1 shuffles;
+// the block value lands in lane 0 (bitwise tree_fold<T>(sm, 256)).
+__device__ __forceinline__ double warp_tree256(double (&v)[8]) {
+#pragma unroll
+    for (int j = 0; j < 4; j++) v[j] = add(v[j], v[j + 4]);
+#pragma unroll
+    for (int j = 0; j < 2; j++) v[j] = add(v[j], v[j + 2]);
+    double r = add(v[0], v[1]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) r = add(r, __shfl_down_sync(0xffffffffu, r, off));
+    return r;
+}
+
+// ---- small n: one thread-block cluster -----------------------------------
+// For n <= S with block_size 256 every slot holds at most one element, so
+// lattice block b is the 256-element chunk b and its value the reference tree
+// over add(+0.0, term) of its slots.  One cluster of C <= 16 CTAs does the
+// whole reduction: CTA r owns blocks r, r + C, ... (at most Q) and stages all
+// of their input chunks in shared memory with 16-byte cp.async (fire and
+// forget -- every load in flight at once, whatever the compiler schedules);
+// then one warp per block computes its slot values and the block's tree in
+// registers and writes the block partial straight into CTA 0's shared memory
+// (DSMEM); after one cluster barrier one warp of CTA 0 runs the second stage.  No global ticket,
+// no partials round trip through L2: at small n that handshake was most of
+// the call (profiles/r01_lattice_latency.md).  Bitwise the same scalar: the
+// same slot values, trees and second-stage order as k_lattice.
+template <int MODE, int Q>
+__global__ void __launch_bounds__(256) k_lattice_cluster(RArgs Ain) {
+    namespace cg = cooperative_groups;
+    constexpr int NA = NArr<MODE>::v;
+    constexpr int AR = Q * 256;  // doubles per staged array
+    RArgs A = Ain;
+    if (!resolve(A)) return;  // the gate is the same for every CTA of the cluster
+    extern __shared__ __align__(16) double stage[];  // NA arrays x [Q][256]
+    __shared__ double parts[512];                    // CTA 0: the block partials
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    const int t = threadIdx.x;
+    const int64_t n = A.n;
+    const int nblk = (int)((n + 255) >> 8);
+    const int nq = min(Q, (nblk - 1 - rank) / C + 1);  // >= 1: the launch has C <= nblk
+    const double *src[4] = {A.u, A.v, A.x, A.r};
+    // stage: 128 sixteen-byte pieces per block chunk, zero-filled past n
+    for (int idx = t; idx < (nq << 7); idx += 256) {
+        const int q = idx >> 7, pc = idx & 127;
+        const int64_t e = ((int64_t)(rank + q * C) << 8) + 2 * pc;
+        if (e >= n) continue;
+        const int bytes = n - e >= 2 ? 16 : 8;
+#pragma unroll
+        for (int a = 0; a < NA; a++) cp_async16_n(stage + a * AR + q * 256 + 2 * pc, src[a] + e, bytes);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    // one warp per block, all in registers: lane l holds slots l + 32j
+    // (j < 8), so the reference tree's levels 128, 64, 32 pair registers of the
+    // same lane (slot s with s + k = l + 32(j + k/32)) and 16..1 are shuffles
+    const int warp = t >> 5, lane = t & 31;
+    double *parts0 = cl.map_shared_rank(parts, 0);
+    for (int q = warp; q < nq; q += 8) {
+        const int64_t b0 = (int64_t)(rank + q * C) << 8;
+        const double *s0 = stage + q * 256 + lane;
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const int64_t i = b0 + lane + 32 * j;
+            v[j] = 0.0;
+            if (i < n) {
+                if constexpr (MODE == R_NORM) {
+                    v[j] = add(0.0, mul(s0[32 * j], s0[32 * j]));
+                } else if constexpr (MODE == R_DOT) {
+                    v[j] = add(0.0, mul(s0[32 * j], s0[AR + 32 * j]));
+                } else {  // x += alpha p ; r -= alpha Ap ; r_new^2 (kernels.py:127-131)
+                    const double xn = add(s0[2 * AR + 32 * j], mul(A.alpha, s0[32 * j]));
+                    const double rn = sub(s0[3 * AR + 32 * j], mul(A.alpha, s0[AR + 32 * j]));
+                    st_stream(A.x + i, xn);
+                    st_stream(A.r + i, rn);
+                    v[j] = add(0.0, mul(rn, rn));
+                }
+            }
+        }
+        const double bv = warp_tree256(v);
+        if (lane == 0) parts0[rank + q * C] = bv;
+    }
+    cl.sync();  // release the DSMEM partials / acquire them in CTA 0
+    if (rank != 0 || warp != 0) return;
+    // second stage (kernels.py:72-81): slot s = 0.0 + parts[s] + parts[s + 256] + ..
+    // over the launched blocks (see k_lattice), then the same tree
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        double acc = 0.0;
+        for (int c = lane + 32 * j; c < nblk; c += 256) acc = add(acc, parts[c]);
+        v[j] = acc;
+    }
+    const double res = warp_tree256(v);
+    if (lane == 0) write_result(A, res);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) k_lattice_global(RArgs Ain) {
     RArgs A = Ain;
@@ -502,6 +604,96 @@ static int64_t tma_min_override() {
         return e && e[0] ? (int64_t)atoll(e) : (int64_t)-1;
     }();
     return v;
+}
+
+// SB200_NO_CLUSTER=1 keeps small calls on k_lattice (A/B checks).
+static bool use_cluster() {
+    static const bool on = [] {
+        const char *e = getenv("SB200_NO_CLUSTER");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
+// Largest cluster the device schedules for k_lattice_cluster (16 when the
+// non-portable size is available, else 8); cached per device.
+template <int MODE, int Q>
+static int cluster_cap(int dev) {
+    static int cap[64];
+    static bool done[64];
+    if (dev < 0 || dev >= 64) return 8;
+    if (done[dev]) return cap[dev];
+    auto kern = k_lattice_cluster<MODE, Q>;
+    const int smem = NArr<MODE>::v * Q * 256 * (int)sizeof(double);
+    int c = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess) {
+        c = 8;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            cfg.gridDim = dim3(16);
+            cfg.blockDim = dim3(256);
+            cfg.dynamicSmemBytes = smem;
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 16;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int active = 0;
+            if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) == cudaSuccess && active > 0) c = 16;
+        }
+    }
+    cudaGetLastError();  // a refused attribute is not a launch error
+    cap[dev] = c;
+    done[dev] = true;
+    return c;
+}
+
+// Launch k_lattice_cluster for BS3/BS4 calls of at most kClusterBlocks
+// lattice blocks (n <= 16384 at block_size 256); returns -1 otherwise.  A
+// cluster streams with at most 16 SMs (~45 GB/s each), so beyond ~16 K
+// elements the whole-GPU k_lattice wins despite its handshake; BS5 (four
+// staged arrays and two store streams per element) was no faster in the
+// cluster at any size (profiles/r01_lattice_latency.md).
+constexpr int kClusterBlocks = 64;
+template <int MODE>
+static int launch_cluster(const RArgs &A, cudaStream_t st, const char *name) {
+    if constexpr (MODE == R_FUSED) {
+        return -1;
+    } else {
+        const int nblk = (int)((A.n + 255) / 256);
+        if (nblk > kClusterBlocks) return -1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int cap = cluster_cap<MODE, 8>(dev);
+        if (cap == 0) return -1;
+        const int C = std::min(cap, nblk);
+        const int need = (nblk + C - 1) / C;  // <= 8
+        int Q = 1;
+        while (Q < need) Q <<= 1;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        cfg.gridDim = dim3((unsigned)C);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = (size_t)NArr<MODE>::v * Q * 256 * sizeof(double);
+        cfg.stream = st;
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)C;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        switch (Q) {
+#define SB_CL(Q_)                                                                               \
+    case Q_:                                                                                    \
+        if (cluster_cap<MODE, Q_>(dev) == 0) return -1; /* sets the kernel's attributes */     \
+        return cuda_check(cudaLaunchKernelEx(&cfg, k_lattice_cluster<MODE, Q_>, A), name);
+            SB_CL(1) SB_CL(2) SB_CL(4) SB_CL(8)
+#undef SB_CL
+            default: return -1;
+        }
+    }
 }
 
 template <int MODE>
@@ -584,13 +776,18 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
 #undef SB_TMA
         return launch_check(name);
     }
+    if (A.bs == 256 && A.n > 0 && A.n <= A.S && use_cluster() && aligned16(A.u) && aligned16(A.v) &&
+        (MODE != R_FUSED || (aligned16(A.x) && aligned16(A.r)))) {
+        const int rc = launch_cluster<MODE>(A, st, name);
+        if (rc >= 0) return rc;
+    }
     // For n < S every lattice block past ceil(n / bs) is empty: its slots
     // stay +0.0, its tree gives +0.0, and adding +0.0 in the final reduce
     // leaves any running sum (which starts at +0.0 and so is never -0.0)
     // unchanged -- launching only the non-empty blocks is bitwise the same
     // and cuts the small-n fixed cost (fewer CTAs on the completion ticket).
     const unsigned grid_lat = A.n < A.S ? (unsigned)std::max<int64_t>(1, (A.n + A.bs - 1) / A.bs) : grid;
-#define SB_LAT(T_, SPT_) k_lattice<T_, SPT_, MODE, U><<<grid_lat, T_, 0, st>>>(A)
+#define SB_LAT(T_, SPT_) k_lattice<T_, SPT_, MODE, (U / SPT_ > 0 ? U / SPT_ : 1)><<<grid_lat, T_, 0, st>>>(A)  /* same bytes in flight per thread */
     switch (A.bs) {
         case 2: SB_LAT(2, 1); break;
         case 4: SB_LAT(4, 1); break;
