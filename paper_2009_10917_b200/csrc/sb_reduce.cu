@@ -14,16 +14,15 @@
 //     all U*streams loads are issued before the U in-order adds.
 //   * Tree: shared memory for levels k >= 32, warp shuffles for 16..1 --
 //     level k adds slot s+k into slot s exactly as `rows[:k] += rows[k:2k]`.
-//   * Single launch: the last CTA to finish (threadfence + atomic ticket)
-//     runs the second stage over the partials and resets the ticket.
+//   * Single launch: every CTA but 0 publishes its block value(s) as flagged
+//     8-byte words (no fence, no atomic); CTA 0 runs the second stage from
+//     them as they arrive and re-zeroes the slots (second_stage below).
 //   * BS5 updates x and r and accumulates r_new^2 in the same pass (48 B/el,
 //     the reference's CPU code re-reads r), on the BS3 lattice, so
 //     bs5 == bs3_norm2(r_new) bitwise (test_kernels.py:194-199).
 #include <stdlib.h>
 
 #include <algorithm>
-
-#include <cooperative_groups.h>
 
 #include "sb_common.cuh"
 #include "sb_lsa.cuh"
@@ -66,7 +65,7 @@ struct RArgs {
     int64_t bs;  // block_size
     int64_t nb;  // n_blocks
     double *partials;
-    unsigned *ticket;
+    unsigned long long *ll;  // flagged partial slots, 16 B per lattice block
     double *result;
     double *lattice;  // generic path only
     // device CG: *gate == 0 -> every CTA returns; alpha read from *alpha_ptr
@@ -92,9 +91,12 @@ __device__ __forceinline__ bool resolve(RArgs &A) {
     return true;
 }
 
-// Workspace layout: [ticket: 256 B][partials: nb doubles][generic: S + bs doubles]
+// Workspace layout: [256 B header (sb_dot_compensated's ticket)][partials:
+// nb doubles (generic path)][flagged partial
+// slots: nb x 16 B][generic path: S + bs doubles].  Zero between calls.
+static size_t ll_offset(int64_t nb) { return (256 + sizeof(double) * (size_t)nb + 15) & ~(size_t)15; }  // 16 B aligned
 static size_t ws_bytes(int64_t bs, int64_t nb) {
-    size_t b = 256 + sizeof(double) * (size_t)nb;
+    size_t b = ll_offset(nb) + 16 * (size_t)nb;
     if (bs > 1024) b += sizeof(double) * ((size_t)bs * (size_t)nb + (size_t)bs);
     return (b + 255) & ~(size_t)255;
 }
@@ -166,30 +168,53 @@ __device__ __forceinline__ double tree_fold(double *sm, int bs) {
     return v;
 }
 
+// Cross-CTA combine of k_lattice without a ticket: every CTA but 0 publishes
+// its block value as two 8-byte words {flag = 1, 32-bit half} (each word is
+// single-copy atomic, so a reader that sees the flag sees its half -- no
+// fence, no atomic), and CTA 0 runs the second stage straight from those
+// slots, spinning on each until it is flagged, then zeroes it for the next
+// call.  One L2 round trip less than release-ticket + re-read; no deadlock
+// risk: only CTA 0 waits, and every other CTA runs to completion without
+// waiting on anything.
+__device__ __forceinline__ void ll_put(unsigned long long *slot, double v) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long hi = (1ull << 32) | (bits >> 32), lo = (1ull << 32) | (bits & 0xffffffffull);
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(hi), "l"(lo) : "memory");
+}
+__device__ __forceinline__ double ll_take(unsigned long long *slot) {
+    unsigned long long hi, lo;
+    for (unsigned polls = 0;; polls++) {
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(hi), "=l"(lo) : "l"(slot) : "memory");
+        if ((hi >> 32) == 1ull && (lo >> 32) == 1ull) break;
+        if (polls >= 4096) __nanosleep(256);
+        // a slot that is never published is a bug: fail the launch (seconds
+        // of polling) instead of hanging the device
+        if (polls == (1u << 24)) __trap();
+    }
+    asm volatile("st.global.v2.u64 [%0], {%1, %1};" ::"l"(slot), "l"(0ull) : "memory");
+    return __longlong_as_double((long long)(((hi & 0xffffffffull) << 32) | (lo & 0xffffffffull)));
+}
+
 template <int T>
 __device__ __forceinline__ void second_stage(const RArgs &A, double *sm, int bs, int spt, double v) {
-    __shared__ bool is_last;
-    if (threadIdx.x == 0) {
-        A.partials[blockIdx.x] = v;
-        is_last = ticket_add(A.ticket) == gridDim.x - 1;
+    if (blockIdx.x != 0) {
+        if (threadIdx.x == 0) ll_put(A.ll + 2 * blockIdx.x, v);
+        return;
     }
-    __syncthreads();
-    if (!is_last) return;
     // _final_reduce (kernels.py:72-81): s[t] = 0.0 + partials[t] + partials[t+bs] + ...
+    // over the launched blocks (see launch_reduce: blocks past n hold +0.0,
+    // and acc + 0.0 == acc for an acc that started at +0.0); partial 0 is
+    // this CTA's own value, held by thread 0 (the owner of slot 0)
     for (int j = 0; j < spt; j++) {
         const int t = threadIdx.x + j * T;
         double acc = 0.0;
-        // only the launched blocks have partials (see launch_reduce: blocks
-        // past n hold +0.0, and acc + 0.0 == acc for an acc that started at +0.0)
-        for (int64_t c = t; c < (int64_t)gridDim.x; c += bs) acc = add(acc, __ldcg(A.partials + c));
+        for (int64_t c = t; c < (int64_t)gridDim.x; c += bs)
+            acc = add(acc, c == 0 ? v : ll_take(A.ll + 2 * c));
         sm[t] = acc;
     }
     __syncthreads();
     const double res = tree_fold<T>(sm, bs);
-    if (threadIdx.x == 0) {
-        write_result(A, res);
-        *A.ticket = 0u;  // workspace left ready for the next call on this stream
-    }
+    if (threadIdx.x == 0) write_result(A, res);
 }
 
 // The last, partial batch of a chain (fewer than U steps left): all of its
@@ -401,142 +426,45 @@ __global__ void __launch_bounds__(T + 32) k_lattice_tma(RArgs Ain) {
         }
         __syncthreads();
     }
+    // block values: CTA 0 keeps its own in shared memory, every other CTA
+    // publishes them as flagged slots (ll_put, see second_stage)
+    __shared__ double own[BPC];
     double v = 0.0;
     if (warp < BPC) {
         constexpr int W = LB < 32 ? LB : 32;
         if (lane < W) v = sm[warp * LB + lane];
         for (int off = W / 2; off >= 1; off >>= 1) v = add(v, __shfl_down_sync(0xffffffffu, v, off));
-        if (lane == 0) A.partials[(int64_t)blockIdx.x * BPC + warp] = v;
+        if (lane == 0) {
+            if (blockIdx.x == 0)
+                own[warp] = v;
+            else
+                ll_put(A.ll + 2 * ((int64_t)blockIdx.x * BPC + warp), v);
+        }
     }
+    if (blockIdx.x != 0) return;
     __syncthreads();
-    // second stage by the last CTA (ticket_add: release of the partials above,
-    // acquire of everyone else's in the last CTA)
-    __shared__ bool is_last;
-    if (tid == 0) is_last = ticket_add(A.ticket) == gridDim.x - 1;
-    __syncthreads();
-    if (!is_last) return;
-    for (int t = tid; t < LB; t += T) {
+    // second stage in CTA 0, straight from the flagged slots; consumer threads
+    // only (the producer warp, tid >= T, would take slots t >= T twice, and a
+    // taken slot is re-zeroed, so the second taker would spin forever)
+    for (int t = tid; t < LB && tid < T; t += T) {
         double a2 = 0.0;
-        for (int64_t c = t; c < A.nb; c += LB) a2 = add(a2, __ldcg(A.partials + c));
+        for (int64_t c = t; c < A.nb; c += LB) a2 = add(a2, c < BPC ? own[c] : ll_take(A.ll + 2 * c));
         sm[t] = a2;
     }
     __syncthreads();
     for (int k = LB / 2; k >= 32; k >>= 1) {
-        for (int s = tid; s < k; s += T) sm[s] = add(sm[s], sm[s + k]);
+        for (int s = tid; s < k && tid < T; s += T) sm[s] = add(sm[s], sm[s + k]);
         __syncthreads();
     }
     if (tid < 32) {
         constexpr int W = LB < 32 ? LB : 32;
         double r = tid < W ? sm[tid] : 0.0;
         for (int off = W / 2; off >= 1; off >>= 1) r = add(r, __shfl_down_sync(0xffffffffu, r, off));
-        if (tid == 0) {
-            write_result(A, r);
-            *A.ticket = 0u;
-        }
+        if (tid == 0) write_result(A, r);
     }
 }
 
 // ---- generic path (block_size > 1024): lattice in global memory ----------
-// The reference tree over 256 slots held by one warp, lane l owning slots
-// l + 32j in v[j]: levels 128, 64, 32 are register adds, 16..1 shuffles;
-// the block value lands in lane 0 (bitwise tree_fold<T>(sm, 256)).
-__device__ __forceinline__ double warp_tree256(double (&v)[8]) {
-#pragma unroll
-    for (int j = 0; j < 4; j++) v[j] = add(v[j], v[j + 4]);
-#pragma unroll
-    for (int j = 0; j < 2; j++) v[j] = add(v[j], v[j + 2]);
-    double r = add(v[0], v[1]);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) r = add(r, __shfl_down_sync(0xffffffffu, r, off));
-    return r;
-}
-
-// ---- small n: one thread-block cluster -----------------------------------
-// For n <= S with block_size 256 every slot holds at most one element, so
-// lattice block b is the 256-element chunk b and its value the reference tree
-// over add(+0.0, term) of its slots.  One cluster of C <= 16 CTAs does the
-// whole reduction: CTA r owns blocks r, r + C, ... (at most Q) and stages all
-// of their input chunks in shared memory with 16-byte cp.async (fire and
-// forget -- every load in flight at once, whatever the compiler schedules);
-// then one warp per block computes its slot values and the block's tree in
-// registers and writes the block partial straight into CTA 0's shared memory
-// (DSMEM); after one cluster barrier one warp of CTA 0 runs the second stage.  No global ticket,
-// no partials round trip through L2: at small n that handshake was most of
-// the call (profiles/r01_lattice_latency.md).  Bitwise the same scalar: the
-// same slot values, trees and second-stage order as k_lattice.
-template <int MODE, int Q>
-__global__ void __launch_bounds__(256) k_lattice_cluster(RArgs Ain) {
-    namespace cg = cooperative_groups;
-    constexpr int NA = NArr<MODE>::v;
-    constexpr int AR = Q * 256;  // doubles per staged array
-    RArgs A = Ain;
-    if (!resolve(A)) return;  // the gate is the same for every CTA of the cluster
-    extern __shared__ __align__(16) double stage[];  // NA arrays x [Q][256]
-    __shared__ double parts[512];                    // CTA 0: the block partials
-    cg::cluster_group cl = cg::this_cluster();
-    const int C = (int)cl.num_blocks(), rank = (int)cl.block_rank();
-    const int t = threadIdx.x;
-    const int64_t n = A.n;
-    const int nblk = (int)((n + 255) >> 8);
-    const int nq = min(Q, (nblk - 1 - rank) / C + 1);  // >= 1: the launch has C <= nblk
-    const double *src[4] = {A.u, A.v, A.x, A.r};
-    // stage: 128 sixteen-byte pieces per block chunk, zero-filled past n
-    for (int idx = t; idx < (nq << 7); idx += 256) {
-        const int q = idx >> 7, pc = idx & 127;
-        const int64_t e = ((int64_t)(rank + q * C) << 8) + 2 * pc;
-        if (e >= n) continue;
-        const int bytes = n - e >= 2 ? 16 : 8;
-#pragma unroll
-        for (int a = 0; a < NA; a++) cp_async16_n(stage + a * AR + q * 256 + 2 * pc, src[a] + e, bytes);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    // one warp per block, all in registers: lane l holds slots l + 32j
-    // (j < 8), so the reference tree's levels 128, 64, 32 pair registers of the
-    // same lane (slot s with s + k = l + 32(j + k/32)) and 16..1 are shuffles
-    const int warp = t >> 5, lane = t & 31;
-    double *parts0 = cl.map_shared_rank(parts, 0);
-    for (int q = warp; q < nq; q += 8) {
-        const int64_t b0 = (int64_t)(rank + q * C) << 8;
-        const double *s0 = stage + q * 256 + lane;
-        double v[8];
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-            const int64_t i = b0 + lane + 32 * j;
-            v[j] = 0.0;
-            if (i < n) {
-                if constexpr (MODE == R_NORM) {
-                    v[j] = add(0.0, mul(s0[32 * j], s0[32 * j]));
-                } else if constexpr (MODE == R_DOT) {
-                    v[j] = add(0.0, mul(s0[32 * j], s0[AR + 32 * j]));
-                } else {  // x += alpha p ; r -= alpha Ap ; r_new^2 (kernels.py:127-131)
-                    const double xn = add(s0[2 * AR + 32 * j], mul(A.alpha, s0[32 * j]));
-                    const double rn = sub(s0[3 * AR + 32 * j], mul(A.alpha, s0[AR + 32 * j]));
-                    st_stream(A.x + i, xn);
-                    st_stream(A.r + i, rn);
-                    v[j] = add(0.0, mul(rn, rn));
-                }
-            }
-        }
-        const double bv = warp_tree256(v);
-        if (lane == 0) parts0[rank + q * C] = bv;
-    }
-    cl.sync();  // release the DSMEM partials / acquire them in CTA 0
-    if (rank != 0 || warp != 0) return;
-    // second stage (kernels.py:72-81): slot s = 0.0 + parts[s] + parts[s + 256] + ..
-    // over the launched blocks (see k_lattice), then the same tree
-    double v[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-        double acc = 0.0;
-        for (int c = lane + 32 * j; c < nblk; c += 256) acc = add(acc, parts[c]);
-        v[j] = acc;
-    }
-    const double res = warp_tree256(v);
-    if (lane == 0) write_result(A, res);
-}
-
 template <int MODE>
 __global__ void __launch_bounds__(256) k_lattice_global(RArgs Ain) {
     RArgs A = Ain;
@@ -606,96 +534,6 @@ static int64_t tma_min_override() {
     return v;
 }
 
-// SB200_NO_CLUSTER=1 keeps small calls on k_lattice (A/B checks).
-static bool use_cluster() {
-    static const bool on = [] {
-        const char *e = getenv("SB200_NO_CLUSTER");
-        return !(e && e[0] == '1');
-    }();
-    return on;
-}
-
-// Largest cluster the device schedules for k_lattice_cluster (16 when the
-// non-portable size is available, else 8); cached per device.
-template <int MODE, int Q>
-static int cluster_cap(int dev) {
-    static int cap[64];
-    static bool done[64];
-    if (dev < 0 || dev >= 64) return 8;
-    if (done[dev]) return cap[dev];
-    auto kern = k_lattice_cluster<MODE, Q>;
-    const int smem = NArr<MODE>::v * Q * 256 * (int)sizeof(double);
-    int c = 0;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess) {
-        c = 8;
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
-            cudaLaunchConfig_t cfg = {};
-            cudaLaunchAttribute at[1];
-            cfg.gridDim = dim3(16);
-            cfg.blockDim = dim3(256);
-            cfg.dynamicSmemBytes = smem;
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = 16;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            int active = 0;
-            if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) == cudaSuccess && active > 0) c = 16;
-        }
-    }
-    cudaGetLastError();  // a refused attribute is not a launch error
-    cap[dev] = c;
-    done[dev] = true;
-    return c;
-}
-
-// Launch k_lattice_cluster for BS3/BS4 calls of at most kClusterBlocks
-// lattice blocks (n <= 16384 at block_size 256); returns -1 otherwise.  A
-// cluster streams with at most 16 SMs (~45 GB/s each), so beyond ~16 K
-// elements the whole-GPU k_lattice wins despite its handshake; BS5 (four
-// staged arrays and two store streams per element) was no faster in the
-// cluster at any size (profiles/r01_lattice_latency.md).
-constexpr int kClusterBlocks = 64;
-template <int MODE>
-static int launch_cluster(const RArgs &A, cudaStream_t st, const char *name) {
-    if constexpr (MODE == R_FUSED) {
-        return -1;
-    } else {
-        const int nblk = (int)((A.n + 255) / 256);
-        if (nblk > kClusterBlocks) return -1;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        const int cap = cluster_cap<MODE, 8>(dev);
-        if (cap == 0) return -1;
-        const int C = std::min(cap, nblk);
-        const int need = (nblk + C - 1) / C;  // <= 8
-        int Q = 1;
-        while (Q < need) Q <<= 1;
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[1];
-        cfg.gridDim = dim3((unsigned)C);
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = (size_t)NArr<MODE>::v * Q * 256 * sizeof(double);
-        cfg.stream = st;
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = (unsigned)C;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        switch (Q) {
-#define SB_CL(Q_)                                                                               \
-    case Q_:                                                                                    \
-        if (cluster_cap<MODE, Q_>(dev) == 0) return -1; /* sets the kernel's attributes */     \
-        return cuda_check(cudaLaunchKernelEx(&cfg, k_lattice_cluster<MODE, Q_>, A), name);
-            SB_CL(1) SB_CL(2) SB_CL(4) SB_CL(8)
-#undef SB_CL
-            default: return -1;
-        }
-    }
-}
-
 template <int MODE>
 static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
     clear_error();
@@ -709,8 +547,8 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
         return SB_E_INVALID;
     }
     char *w = static_cast<char *>(ws);
-    A.ticket = reinterpret_cast<unsigned *>(w);
     A.partials = reinterpret_cast<double *>(w + 256);
+    A.ll = reinterpret_cast<unsigned long long *>(w + ll_offset(A.nb));
     A.S = A.bs * A.nb;
     const unsigned grid = (unsigned)A.nb;
     // U (chain unroll) is chosen so the batch keeps >= ~128 B in flight per
@@ -776,16 +614,11 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
 #undef SB_TMA
         return launch_check(name);
     }
-    if (A.bs == 256 && A.n > 0 && A.n <= A.S && use_cluster() && aligned16(A.u) && aligned16(A.v) &&
-        (MODE != R_FUSED || (aligned16(A.x) && aligned16(A.r)))) {
-        const int rc = launch_cluster<MODE>(A, st, name);
-        if (rc >= 0) return rc;
-    }
     // For n < S every lattice block past ceil(n / bs) is empty: its slots
     // stay +0.0, its tree gives +0.0, and adding +0.0 in the final reduce
     // leaves any running sum (which starts at +0.0 and so is never -0.0)
     // unchanged -- launching only the non-empty blocks is bitwise the same
-    // and cuts the small-n fixed cost (fewer CTAs on the completion ticket).
+    // and cuts the small-n fixed cost (fewer partials for CTA 0 to collect).
     const unsigned grid_lat = A.n < A.S ? (unsigned)std::max<int64_t>(1, (A.n + A.bs - 1) / A.bs) : grid;
 #define SB_LAT(T_, SPT_) k_lattice<T_, SPT_, MODE, (U / SPT_ > 0 ? U / SPT_ : 1)><<<grid_lat, T_, 0, st>>>(A)  /* same bytes in flight per thread */
     switch (A.bs) {
@@ -800,7 +633,7 @@ static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
         case 512: SB_LAT(256, 2); break;
         case 1024: SB_LAT(256, 4); break;
         default: {
-            A.lattice = reinterpret_cast<double *>(w + 256 + sizeof(double) * (size_t)A.nb);
+            A.lattice = reinterpret_cast<double *>(w + ll_offset(A.nb) + 16 * (size_t)A.nb);
             const int64_t want = (A.S + 255) / 256;
             const unsigned g = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 8);
             k_lattice_global<MODE><<<g, 256, 0, st>>>(A);
