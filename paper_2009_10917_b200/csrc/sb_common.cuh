@@ -64,15 +64,6 @@ int cg_pap_impl(const double *p, const double *ap, int64_t n, int64_t bs, int64_
 int cg_update_impl(int fused, const double *p, const double *ap, double *x, double *r, int64_t n, int64_t bs,
                    int64_t nb, void *ws, sb_cg_state *st, const LsaArgs *lsa, cudaStream_t s);
 
-// Completion ticket of single-launch reductions: a gpu-scope acq_rel add.  The
-// release publishes this CTA's partials (written before the preceding
-// __syncthreads, cumulative through the barrier); the acquire in the last CTA
-// orders its reads of every other CTA's partials -- no separate fences.
-__device__ __forceinline__ unsigned ticket_add(unsigned *t) {
-    unsigned prev;
-    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(t) : "memory");
-    return prev;
-}
 
 // ---- cache-policy helpers: HBM streams are touched once -> evict-first.
 __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
