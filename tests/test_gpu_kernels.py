@@ -312,3 +312,22 @@ print(" ".join(out))
         assert r.returncode == 0, r.stderr[-2000:]
         res.append(r.stdout.strip())
     assert res[0] == res[1]
+
+
+@pytest.mark.parametrize("n", [1, 1000, 131073, 3_000_017, 20_000_003])
+def test_reduction_workspace_left_zeroed(sb, n):
+    """include/sb200.h: a reduction leaves its workspace zeroed for the next
+    call on the stream -- CTA 0 re-zeroes every flagged partial slot it
+    collects (register lattice and TMA ring alike; BS5 takes the ring from
+    3 M elements, BS3/BS4 stay on the register lattice here)."""
+    from paper_2009_10917_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    y = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    for cfg in (sb.ReductionConfig(), sb.ReductionConfig(512, 296), sb.ReductionConfig(64, 7)):
+        first = (sb.bs3_norm2(x, cfg), sb.bs4_dot(x, y, cfg))
+        sb.bs5_fused_cg_update(0.0, y, x, x.clone(), y.clone(), cfg)
+        torch.cuda.synchronize()
+        ws = _lib.workspace(x.device, _lib.stream_handle(x.device), cfg.block_size, cfg.n_blocks)
+        assert int(torch.count_nonzero(ws)) == 0, (n, cfg)
+        assert (sb.bs3_norm2(x, cfg), sb.bs4_dot(x, y, cfg)) == first
