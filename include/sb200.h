@@ -240,7 +240,7 @@ int sb_cg_direction(const double *r, double *p, int64_t n, sb_cg_state *state,
 
 
 /* ---- fused multi-GPU reductions -----------------------
- * BS3/BS4/BS5 whose last CTA also combines the per-rank scalars over NVLink
+ * BS3/BS4/BS5 whose CTA 0 also combines the per-rank scalars over NVLink
  * peer memory (NCCL 2.28 device API, LSA windows): the rank's value is
  * stored into every peer's symmetric window, the ranks meet at an LSA
  * barrier, and each sums the values in rank order from +0.0 -- bitwise the
@@ -249,6 +249,10 @@ int sb_cg_direction(const double *r, double *p, int64_t n, sb_cg_state *state,
  * context.  Needs libnccl.so.2 >= 2.28 in the process (torch's) and every
  * rank NVLink-reachable; otherwise sb_lsa_create returns SB_E_INVALID. */
 typedef struct sb_lsa sb_lsa_t;
+/* SB_OK when this process can attempt the fused path (libnccl.so.2 >= 2.28
+ * with the host symbols loadable); local, non-collective, no side effects --
+ * ranks agree on it before the collective sb_lsa_create. */
+int sb_lsa_available(void);
 int sb_lsa_unique_id(void *out, size_t bytes);  /* rank 0; bytes >= 128 */
 int sb_lsa_create(const void *unique_id, size_t bytes, int nranks, int rank, sb_lsa_t **out);
 int sb_lsa_destroy(sb_lsa_t *ctx);

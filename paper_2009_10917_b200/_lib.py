@@ -69,6 +69,7 @@ _SIGS = {
     "sb_cg_update": (_c_int, [_c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp,
                               _c_vp]),
     "sb_cg_direction": (_c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_vp]),
+    "sb_lsa_available": (_c_int, []),
     "sb_lsa_unique_id": (_c_int, [_c_vp, _c_size]),
     "sb_lsa_create": (_c_int, [_c_vp, _c_size, _c_int, _c_int, _c_vp]),
     "sb_lsa_destroy": (_c_int, [_c_vp]),

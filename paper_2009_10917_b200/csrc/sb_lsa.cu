@@ -117,6 +117,11 @@ static void lsa_free(sb_lsa_t *c) {
 
 extern "C" {
 
+int sb_lsa_available(void) {
+    clear_error();
+    return need_api("sb_lsa_available");
+}
+
 int sb_lsa_unique_id(void *out, size_t bytes) {
     clear_error();
     if (int rc = need_api("sb_lsa_unique_id")) return rc;

@@ -397,12 +397,20 @@ class BenchContext:
         if use_lsa is None:
             use_lsa = _nccl(None) and os.environ.get("SB200_LSA", "1") != "0"
         if use_lsa:
-            from .lsa import LsaReducer, LsaUnavailable
-            why = None
-            try:
-                self.lsa = LsaReducer(world, rank, device)
-            except LsaUnavailable as e:
-                why = str(e)
+            from . import lsa as _lsa
+            # first agree that every rank can even try (local checks), so no
+            # rank enters NCCL's collective setup alone; then agree on success
+            why = _lsa.capable(world, device)
+            can = torch.tensor([0 if why else 1], dtype=torch.int32, device=self.device)
+            if world > 1:
+                dist.all_reduce(can, op=dist.ReduceOp.MIN)
+            if int(can.item()) == 1:
+                try:
+                    self.lsa = _lsa.LsaReducer(world, rank, device)
+                except _lsa.LsaUnavailable as e:
+                    why = str(e)
+            elif why is None:
+                why = "another rank cannot set it up"
             # every rank must take the same path (the fused kernels are collective)
             ok = torch.tensor([0 if self.lsa is None else 1], dtype=torch.int32, device=self.device)
             if world > 1:

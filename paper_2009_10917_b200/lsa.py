@@ -30,6 +30,27 @@ class LsaUnavailable(RuntimeError):
     """The fused path cannot be set up here (NCCL < 2.28, ranks not NVLink peers, ...)."""
 
 
+def capable(world: int, device) -> str | None:
+    """Local, non-collective check that this rank can attempt the fused path;
+    None if it can, else why not.  Ranks agree on the answer (all-reduce MIN)
+    before the collective setup, so a rank that cannot even try never leaves
+    the others waiting inside NCCL.  Assumes the launcher's rank r -> local
+    GPU r mapping (one node, torchrun LOCAL_RANK)."""
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        return "not a CUDA device"
+    if _lib.lib().sb_lsa_available() != _lib.SB_OK:
+        return _lib.last_error()
+    n = torch.cuda.device_count()
+    if world > n:
+        return f"{world} ranks but {n} local GPUs (the fused path needs one NVLink domain)"
+    me = dev.index if dev.index is not None else torch.cuda.current_device()
+    for j in range(world):
+        if j != me and not torch.cuda.can_device_access_peer(me, j):
+            return f"GPU {me} has no peer access to GPU {j}"
+    return None
+
+
 class LsaReducer:
     def __init__(self, world: int, rank: int, device, group=None, unique_id: bytes | None = None):
         self.L = _lib.lib()

@@ -159,6 +159,7 @@ def _agree_worker(rank, world, port, fail_rank, results):
                 closed.append(True)
 
         LSA.LsaReducer = FakeLsa
+        LSA.capable = lambda world, device: None  # every rank passes the local checks
         ctx = D.BenchContext(rank, world, types.SimpleNamespace(K=4, order=2), "cpu", use_lsa=True)
         results[rank] = (ctx.lsa is None, "unavailable" in ctx.collective, bool(closed) or rank == fail_rank)
     finally:
@@ -171,5 +172,37 @@ def test_fused_path_agreement_falls_back_on_every_rank(fail_rank):
     mgr = mp.Manager()
     results = mgr.dict()
     mp.spawn(_agree_worker, args=(world, _free_port(), fail_rank, results), nprocs=world, join=True)
+    for r in range(world):
+        assert results[r] == (True, True, True), (r, results[r])
+
+
+def _capable_worker(rank, world, port, fail_rank, results):
+    """A rank that fails the local capability check keeps EVERY rank out of
+    the collective setup (nobody constructs the NVLink context)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2009_10917_b200 import lsa as LSA
+        built = []
+
+        class FakeLsa:
+            def __init__(self, *a, **k):
+                built.append(True)
+
+        LSA.LsaReducer = FakeLsa
+        LSA.capable = lambda world, device: "simulated: no peer access" if rank == fail_rank else None
+        ctx = D.BenchContext(rank, world, types.SimpleNamespace(K=4, order=2), "cpu", use_lsa=True)
+        results[rank] = (ctx.lsa is None, not built, "unavailable" in ctx.collective)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [0, 1])
+def test_capability_check_keeps_every_rank_out(fail_rank):
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_capable_worker, args=(world, _free_port(), fail_rank, results), nprocs=world, join=True)
     for r in range(world):
         assert results[r] == (True, True, True), (r, results[r])
