@@ -67,11 +67,16 @@ class LsaReducer:
         self._ws = {}
 
     def _exchange_uid(self, group) -> bytes:
+        # an all-zero id is the "rank 0 failed" sentinel: every rank still
+        # joins the broadcast and then raises, instead of waiting in it
         t = torch.zeros(UID_BYTES, dtype=torch.uint8)
+        why = ""
         if self.rank == 0:
             raw = ctypes.create_string_buffer(UID_BYTES)
-            _lib.check(self.L.sb_lsa_unique_id(raw, UID_BYTES), "sb_lsa_unique_id")
-            t = torch.frombuffer(bytearray(raw.raw), dtype=torch.uint8).clone()
+            if self.L.sb_lsa_unique_id(raw, UID_BYTES) == _lib.SB_OK:
+                t = torch.frombuffer(bytearray(raw.raw), dtype=torch.uint8).clone()
+            else:
+                why = _lib.last_error()
         if self.world > 1:
             if dist.get_backend(group) == "nccl":
                 td = t.to(self.device)
@@ -79,6 +84,8 @@ class LsaReducer:
                 t = td.cpu()
             else:
                 dist.broadcast(t, 0, group=group)
+        if not bool(t.any()):
+            raise LsaUnavailable(f"rank 0 could not create an NCCL unique id {why}".strip())
         return bytes(t.numpy().tobytes())
 
     @staticmethod
