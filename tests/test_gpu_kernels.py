@@ -256,8 +256,8 @@ print("ok")
 '''
 
 
-@pytest.mark.parametrize("tma_min", ["", "0"])
-@pytest.mark.parametrize("n", [6_000_000, 6_000_001, 7_340_033, 12_582_917])
+@pytest.mark.parametrize("n,tma_min", [(n, t) for n in (6_000_000, 6_000_001, 7_340_033, 12_582_917)
+                                         for t in ("", "0")] + [(n, "0") for n in (1, 1000, 131_073)])
 def test_tma_ring_sizes_and_configs_vs_oracle(n, tma_min):
     """Both lattice kernels at ragged sizes, bitwise the lattice oracle: the
     default crossovers (register lattice for BS3/BS4 here, its ragged last
