@@ -106,3 +106,17 @@ def test_gather_scatter_operator_cg(K, p):
     assert h.converged and d.iterations == h.iterations and torch.equal(d.x, h.x)
     res = (A(d.x) - b).norm() / b.norm()
     assert res.item() < 1e-9
+
+
+def test_host_array_operators_capturable():
+    """Operators built from host numpy arrays (the reference's usage,
+    cg.py:75-92) keep one device copy, so the CUDA-graph device CG can
+    capture them; iterates equal the host-scalar solver's."""
+    from paper_2009_10917_b200 import cg
+    rng = np.random.default_rng(12)
+    for op, n in ((cg.diagonal_operator(np.repeat([1.0, 2.0, 3.0], 8)), 24),
+                  (cg.dense_spd_operator(cg.random_spd_matrix(40, seed=13)), 40)):
+        b = _dev(rng.uniform(-1, 1, n))
+        h = cg.cg_solve(op, b, torch.zeros_like(b), 1e-24, 200)
+        d = cg.cg_solve_device(op, b, torch.zeros_like(b), 1e-24, 200, check_every=2, graph=True)
+        assert d.iterations == h.iterations and torch.equal(d.x, h.x)
