@@ -255,7 +255,10 @@ typedef struct sb_lsa sb_lsa_t;
 int sb_lsa_available(void);
 int sb_lsa_unique_id(void *out, size_t bytes);  /* rank 0; bytes >= 128 */
 int sb_lsa_create(const void *unique_id, size_t bytes, int nranks, int rank, sb_lsa_t **out);
-int sb_lsa_destroy(sb_lsa_t *ctx);
+int sb_lsa_destroy(sb_lsa_t *ctx);  /* collective (every rank of the context) */
+/* Local, non-collective teardown (ncclCommAbort) for a context whose peers
+ * did not all finish sb_lsa_create. */
+int sb_lsa_abort(sb_lsa_t *ctx);
 /* BS6 carry halo over NVLink (dist.py DistGather): a symmetric window per
  * context (collective); sb_lsa_halo_pointers returns this rank's local
  * address of `offset` and peer `peer`'s NVLink-mapped address of it, so the

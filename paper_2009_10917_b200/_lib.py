@@ -73,6 +73,7 @@ _SIGS = {
     "sb_lsa_unique_id": (_c_int, [_c_vp, _c_size]),
     "sb_lsa_create": (_c_int, [_c_vp, _c_size, _c_int, _c_int, _c_vp]),
     "sb_lsa_destroy": (_c_int, [_c_vp]),
+    "sb_lsa_abort": (_c_int, [_c_vp]),
     "sb_lsa_halo_window": (_c_int, [_c_vp, _c_size]),
     "sb_lsa_halo_pointers": (_c_int, [_c_vp, _c_size, _c_int, _c_vp, _c_vp]),
     "sb_lsa_barrier": (_c_int, [_c_vp, _c_vp]),

@@ -18,6 +18,7 @@ struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId *);
     ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
     ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*CommAbort)(ncclComm_t);
     ncclResult_t (*MemAlloc)(void **, size_t);
     ncclResult_t (*MemFree)(void *);
     ncclResult_t (*CommWindowRegister)(ncclComm_t, void *, size_t, ncclWindow_t *, int);
@@ -39,6 +40,7 @@ static NcclApi &nccl_api() {
         SB_SYM(GetUniqueId);
         SB_SYM(CommInitRank);
         SB_SYM(CommDestroy);
+        SB_SYM(CommAbort);
         SB_SYM(MemAlloc);
         SB_SYM(MemFree);
         SB_SYM(CommWindowRegister);
@@ -49,7 +51,7 @@ static NcclApi &nccl_api() {
         SB_SYM(GetErrorString);
         SB_SYM(GetVersion);
 #undef SB_SYM
-        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.MemAlloc && a.MemFree &&
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.CommAbort && a.MemAlloc && a.MemFree &&
                a.CommWindowRegister && a.CommWindowDeregister && a.DevCommCreate && a.DevCommDestroy &&
                a.TeamLsa && a.GetErrorString && a.GetVersion;
         return a;
@@ -180,6 +182,19 @@ int sb_lsa_create(const void *uid, size_t bytes, int nranks, int rank, sb_lsa_t 
         return rc;
     }
     *out = c;
+    return SB_OK;
+}
+
+// Local teardown for when the ranks disagree (some failed sb_lsa_create):
+// no collective call (window deregistration / device-communicator destroy
+// may wait for peers that never registered), just ncclCommAbort; the small
+// symmetric buffers are left to process exit.
+int sb_lsa_abort(sb_lsa_t *ctx) {
+    clear_error();
+    if (!ctx) return SB_OK;
+    cudaDeviceSynchronize();
+    if (ctx->comm) nccl_api().CommAbort(ctx->comm);
+    delete ctx;
     return SB_OK;
 }
 

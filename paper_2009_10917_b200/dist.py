@@ -419,7 +419,7 @@ class BenchContext:
                 self.collective = "fused in-kernel combine over NVLink (NCCL device API, LSA window)"
             else:
                 if self.lsa is not None:
-                    self.lsa.close()
+                    self.lsa.abort()  # local: some peer never built its context
                     self.lsa = None
                 self.collective += f" (fused path unavailable: {why or 'not on every rank'})"
         Kg = max(world, int(round(args.K * world ** (1.0 / 3.0))))

@@ -95,8 +95,15 @@ class LsaReducer:
         return raw.raw
 
     def close(self) -> None:
+        """Collective teardown: every rank of the context calls it."""
         if getattr(self, "handle", None) is not None and self.handle.value:
             self.L.sb_lsa_destroy(self.handle)
+            self.handle = None
+
+    def abort(self) -> None:
+        """Local teardown (ncclCommAbort) when not every rank built its context."""
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self.L.sb_lsa_abort(self.handle)
             self.handle = None
 
     def __del__(self):

@@ -158,6 +158,9 @@ def _agree_worker(rank, world, port, fail_rank, results):
             def close(self):
                 closed.append(True)
 
+            def abort(self):
+                closed.append(True)
+
         LSA.LsaReducer = FakeLsa
         LSA.capable = lambda world, device: None  # every rank passes the local checks
         ctx = D.BenchContext(rank, world, types.SimpleNamespace(K=4, order=2), "cpu", use_lsa=True)

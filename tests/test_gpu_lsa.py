@@ -183,3 +183,17 @@ def test_dist_mass_operator_and_cg_one_rank(lsa):
         assert got.iterations == want.iterations and torch.equal(got.x, want.x)
     finally:
         ctx.close()
+
+
+def test_abort_is_local_and_leaves_the_device_usable():
+    """LsaReducer.abort (the fallback when peers disagree) tears a context
+    down without collective calls; a fresh context then works normally."""
+    from paper_2009_10917_b200 import lsa as LSA
+    r = LSA.LsaReducer(1, 0, "cuda:0", unique_id=LSA.LsaReducer.unique_id())
+    r.abort()
+    assert r.handle is None
+    r2 = LSA.LsaReducer(1, 0, "cuda:0", unique_id=LSA.LsaReducer.unique_id())
+    x = _v(4097, 21)
+    import paper_2009_10917_b200 as sb
+    assert r2.bs3_norm2(x) == 0.0 + sb.bs3_norm2(x)
+    r2.close()
