@@ -33,6 +33,17 @@ def test_run_sweep_all_tests(sb, timer):
         assert [(s.K, s.order) for s in out] == plan.sizes
 
 
+@pytest.mark.parametrize("timer", ["host", "device"])
+def test_run_sweep_sync_scalars(sb, timer):
+    """sync_scalars=True reads every BS3-BS5 scalar back inside the timed
+    batch (the reference API's float return); same samples, validated."""
+    from paper_2009_10917_b200 import harness
+    for test in ("bs3", "bs4", "bs5"):
+        plan = harness.SweepPlan(test=test, sizes=[7, 131073], trials=3, warmup=1)
+        out = harness.run_sweep(plan, timer=timer, sync_scalars=True)
+        assert [s.n for s in out] == plan.sizes and all(s.bandwidth > 0 for s in out)
+
+
 def test_sweep_failure_keeps_samples(sb, monkeypatch):
     """harness.py:256-267: a validation failure aborts with the samples so far."""
     from paper_2009_10917_b200 import harness
