@@ -178,7 +178,11 @@ int sb_lsa_create(const void *uid, size_t bytes, int nranks, int rank, sb_lsa_t 
     }
     if (!rc) rc = cuda_check(cudaDeviceSynchronize(), "sb_lsa_create");
     if (rc) {
-        lsa_free(c);
+        // local teardown: the peers may be anywhere in the setup, so no
+        // collective deregistration (it could wait for a rank that failed
+        // before registering); the small symmetric buffers are left to exit
+        if (c->comm) a.CommAbort(c->comm);
+        delete c;
         return rc;
     }
     *out = c;
