@@ -331,3 +331,24 @@ def test_reduction_workspace_left_zeroed(sb, n):
         ws = _lib.workspace(x.device, _lib.stream_handle(x.device), cfg.block_size, cfg.n_blocks)
         assert int(torch.count_nonzero(ws)) == 0, (n, cfg)
         assert (sb.bs3_norm2(x, cfg), sb.bs4_dot(x, y, cfg)) == first
+
+
+def test_concurrent_streams_own_workspaces(sb):
+    """Reductions on two streams at once (each stream has its own workspace,
+    so each launch's CTA 0 collects only its own flagged slots): every
+    result equals the same call made alone."""
+    g = torch.Generator(device="cuda").manual_seed(77)
+    xs = [torch.rand(n, dtype=torch.float64, device="cuda", generator=g) for n in (5000, 700_001, 3_100_000)]
+    want = [(sb.bs3_norm2(x), sb.bs4_dot(x, x.flip(0))) for x in xs]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    got = {}
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for i, x in enumerate(xs):
+            for k, st in enumerate((s1, s2)):
+                with torch.cuda.stream(st):
+                    y = x.flip(0)
+                    got[(rep, i, k)] = (sb.kernels.bs3_norm2_async(x), sb.kernels.bs4_dot_async(x, y))
+    torch.cuda.synchronize()
+    for (rep, i, k), (a, b) in got.items():
+        assert (float(a.item()), float(b.item())) == want[i], (rep, i, k)
