@@ -110,6 +110,20 @@ struct SbMeta {
     int32_t r0, e0, r1, e1;
 };
 
+// Kernel super-block i = PS consecutive plan super-blocks (rows never split:
+// plan boundaries are operator-block boundaries); nsbk = ceil(nsb / PS).
+template <int PS>
+__device__ __forceinline__ SbMeta load_meta_ps(const int32_t *plan, int64_t i, int64_t nsbk, int64_t nsb) {
+    SbMeta m{0, 0, 0, 0};
+    if (i < nsbk) {
+        const int64_t j = PS * i + PS < nsb ? PS * i + PS : nsb;
+        const int2 lo = __ldg(reinterpret_cast<const int2 *>(plan + 2 * PS * i));
+        const int2 hi = __ldg(reinterpret_cast<const int2 *>(plan + 2 * j));
+        m = SbMeta{lo.x, lo.y, hi.x, hi.y};
+    }
+    return m;
+}
+
 __device__ __forceinline__ SbMeta load_meta(const int32_t *plan, int64_t i, int64_t nsb) {
     SbMeta m{0, 0, 0, 0};
     if (i < nsb) {
@@ -237,7 +251,7 @@ __device__ __forceinline__ void bs6_publish_vals(const SbMeta &m, const double2 
 // and (2t+2T, 2t+2T+1) of its super-block, gathered with one 16 B load when
 // the two columns are adjacent (the 8-entry rows of p = 1 meshes pair up
 // often enough for that to beat one entry per lane).
-template <int T, int CAP, bool SWZ, int MINB = kBs6MinCtas>
+template <int T, int CAP, bool SWZ, int MINB = kBs6MinCtas, int PS = 1>
 __global__ void __launch_bounds__(T, MINB) k_bs6_pairs(const int32_t *__restrict__ plan, int64_t nsb,
                                                              const int32_t *__restrict__ rs,
                                                              const int32_t *__restrict__ ci,
@@ -248,19 +262,20 @@ __global__ void __launch_bounds__(T, MINB) k_bs6_pairs(const int32_t *__restrict
     extern __shared__ __align__(16) unsigned char bs6_smem[];
     double(*qs)[CAP] = reinterpret_cast<double(*)[CAP]>(bs6_smem);
     const int64_t g = gridDim.x;
+    const int64_t nsbk = (nsb + PS - 1) / PS;
     int64_t sbi = blockIdx.x;
-    if (sbi >= nsb) return;
+    if (sbi >= nsbk) return;
     int2 cols[M];
     double2 v[M];
     Bs6Rows<T, CAP> rw;
     int buf = 0;
-    SbMeta mc = load_meta(plan, sbi, nsb), mn = load_meta(plan, sbi + g, nsb);
+    SbMeta mc = load_meta_ps<PS>(plan, sbi, nsbk, nsb), mn = load_meta_ps<PS>(plan, sbi + g, nsbk, nsb);
     bs6_issue_cols<T, CAP>(mc, ci, cols);
-    for (; sbi < nsb; sbi += g) {
+    for (; sbi < nsbk; sbi += g) {
         bs6_issue_vals<T, CAP, SWZ>(mc, cols, q, v);  // A: values of this super-block
         bs6_load_rows<T, CAP>(mc, rs, rw);             // B: its row starts
         bs6_issue_cols<T, CAP>(mn, ci, cols);          // C: indices of the next one
-        const SbMeta mnn = load_meta(plan, sbi + 2 * g, nsb);
+        const SbMeta mnn = load_meta_ps<PS>(plan, sbi + 2 * g, nsbk, nsb);
         bs6_publish_vals<T, CAP, SWZ>(mc, v, qs[buf]);
         __syncthreads();
         bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
@@ -377,15 +392,17 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
                            const double *, int64_t);
     // Kernel, value-tile swizzle and CTAs per SM by the mean row length
     // rho = nl/ng (measured on B200 over N = 1..15, profiles/r01_bs6_variants.md):
-    //   rho >= 4    (p = 1)   pairs, swizzled, 12 CTAs/SM (40 registers)
+    //   rho >= 4    (p = 1)   pairs, swizzled, 1024-entry super-blocks (two
+    //                         plan super-blocks each), 6 CTAs/SM (+6% over
+    //                         512 entries at 12/SM)
     //   rho >= 3    (p = 2)   lanes, plain,    12 CTAs/SM
     //   rho >= 2.2  (p = 3)   lanes, swizzled,  8 CTAs/SM (64 registers)
     //   rho <  2.2  (p >= 4)  lanes, plain,    10 CTAs/SM (48 registers)
-    // SB200_BS6_CFG="<lanes|pairs>,<swizzle 0|1>,<CTAs/SM 6|8|10|12>" overrides
+    // SB200_BS6_CFG="<lanes|pairs|wide>,<swizzle 0|1>,<CTAs/SM 6|8|10|12>" overrides
     // the choice (A/B runs, scripts/expt/time_bs6.py).
-    bool pairs, sw;
+    bool pairs, sw, wide = false;
     int mb;
-    if (nl >= 4 * ng) { pairs = true; sw = true; mb = 12; }
+    if (nl >= 4 * ng) { pairs = true; sw = true; mb = 6; wide = true; }
     else if (nl >= 3 * ng) { pairs = false; sw = false; mb = 12; }
     else if (5 * nl >= 11 * ng) { pairs = false; sw = true; mb = 8; }
     else { pairs = false; sw = false; mb = 10; }
@@ -393,7 +410,8 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     if (cfg && cfg[0] == 'r' && cfg[1] == 'o' && cfg[2] == 'w' && cfg[3] == 's')
         return bs6_rows_launch(rs, ci, ng, q, out, carry, ncarry, as_stream(s));
     if (cfg) {
-        pairs = cfg[0] == 'p';
+        wide = cfg[0] == 'w';  // "wide": the 1024-entry pairs kernel
+        pairs = cfg[0] == 'p' || wide;
         const char *c1 = strchr(cfg, ',');
         sw = c1 && c1[1] == '1';
         const char *c2 = c1 ? strchr(c1 + 1, ',') : nullptr;
@@ -406,6 +424,18 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, T, smem);
         return (unsigned)std::max<int64_t>(1, std::min<int64_t>(nsb, (int64_t)sm_count() * std::max(1, per_sm)));
     };
+    if (wide) {
+        constexpr int CAPW = 2 * kBs6Cap;
+        const size_t smemw = 2 * CAPW * sizeof(double);
+        const KernT kw = sw ? k_bs6_pairs<T, CAPW, true, 6, 2> : k_bs6_pairs<T, CAPW, false, 6, 2>;
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)kw, T, smemw);
+        const int64_t nsbk = (nsb + 1) / 2;
+        const unsigned grid =
+            (unsigned)std::max<int64_t>(1, std::min<int64_t>(nsbk, (int64_t)sm_count() * std::max(1, per_sm)));
+        kw<<<grid, T, smemw, as_stream(s)>>>(plan, nsb, rs, ci, q, out, carry, ncarry);
+        return launch_check("sb_bs6_gather_planned");
+    }
     const KernT kern = pairs ? SB_PICK_MB(k_bs6_pairs) : SB_PICK_MB(k_bs6_lanes);
     kern<<<grid_for((const void *)kern), T, smem, as_stream(s)>>>(plan, nsb, rs, ci, q, out, carry, ncarry);
 #undef SB_PICK_MB
