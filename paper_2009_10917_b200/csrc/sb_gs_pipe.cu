@@ -393,8 +393,9 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     // Kernel, value-tile swizzle and CTAs per SM by the mean row length
     // rho = nl/ng (measured on B200 over N = 1..15, profiles/r01_bs6_variants.md):
     //   rho >= 4    (p = 1)   pairs, swizzled, 1024-entry super-blocks (two
-    //                         plan super-blocks each), 6 CTAs/SM (+6% over
-    //                         512 entries at 12/SM)
+    //                         plan super-blocks each), 6 CTAs/SM (+3-6% over
+    //                         512 entries at 12/SM) once the operator fills
+    //                         two waves of them; else 512 entries, 12/SM
     //   rho >= 3    (p = 2)   lanes, plain,    12 CTAs/SM
     //   rho >= 2.2  (p = 3)   lanes, swizzled,  8 CTAs/SM (64 registers)
     //   rho <  2.2  (p >= 4)  lanes, plain,    10 CTAs/SM (48 registers)
@@ -402,7 +403,12 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     // the choice (A/B runs, scripts/expt/time_bs6.py).
     bool pairs, sw, wide = false;
     int mb;
-    if (nl >= 4 * ng) { pairs = true; sw = true; mb = 6; wide = true; }
+    if (nl >= 4 * ng) {
+        // wide only when every SM gets at least two of its super-blocks: on
+        // small operators half as many CTAs is a longer critical path
+        pairs = true; sw = true; mb = 12;
+        wide = nsb >= 2 * 2 * 6 * (int64_t)sm_count();
+    }
     else if (nl >= 3 * ng) { pairs = false; sw = false; mb = 12; }
     else if (5 * nl >= 11 * ng) { pairs = false; sw = true; mb = 8; }
     else { pairs = false; sw = false; mb = 10; }
