@@ -194,9 +194,12 @@ def test_reference_numpy_operator_drop_in(sb, golden):
     assert np.array_equal(out, arr[f"bs6_{tag}"])
 
 
-@pytest.mark.parametrize("K,p,npb", [(20, 7, 512), (13, 2, 16), (7, 15, 2048), (25, 1, 64), (3, 3, 8)])
+@pytest.mark.parametrize("K,p,npb", [(20, 7, 512), (13, 2, 16), (7, 15, 2048), (25, 1, 64), (3, 3, 8),
+                                     (80, 1, 512), (79, 1, 512), (64, 1, 256)])
 def test_pipelined_bs6_matches_unplanned(sb, K, p, npb):
-    """sb_bs6_gather_planned (persistent, cp.async pipeline) == sb_bs6_gather, with carry."""
+    """sb_bs6_gather_planned (persistent, cp.async pipeline) == sb_bs6_gather, with carry.
+    The p = 1 meshes from K = 64 on take the 1024-entry (two plan
+    super-blocks) kernel, odd and even plan lengths included."""
     import types
     from paper_2009_10917_b200.gs import bs6_gather_into
     mesh = sb.build_mesh(K, p)
