@@ -98,6 +98,9 @@ class GatherOp:
     col_ids: torch.Tensor = field(repr=False)
     block_starts: torch.Tensor = field(repr=False)
     nodes_per_block: int
+    # (K, p, z0, z1, c_lo, c_hi) when the operator is the closed-form CSR of a
+    # build_mesh numbering (or a slab of it): enables the TMA-staged BS6 plan
+    geometry: tuple | None = field(default=None, repr=False, compare=False)
 
     @property
     def nl(self) -> int:
@@ -143,6 +146,39 @@ class GatherOp:
                                               p.data_ptr(), _lib.stream_handle(dev)), "bs6 plan")
         object.__setattr__(self, "_plan", p)
         return p
+
+
+    def staged(self):
+        """(sb_bs6_staged_t, plan) of the TMA-staged BS6 kernel
+        (csrc/sb_gs_staged.cu), built once per operator; None unless the
+        operator is a structured one of order p <= 2 on the device.  Opt-in
+        (SB200_BS6_STAGED=1): measured slower than the super-block kernel so
+        far (profiles/r02_bs6_staged.md); SB200_BS6_TILE="ey,ez,w" overrides
+        the tile shape (A/B runs)."""
+        st = self.__dict__.get("_staged", False)
+        if st is not False:
+            return st
+        st = None
+        geo = self.geometry
+        if (geo is not None and os.environ.get("SB200_BS6_STAGED", "0") == "1"
+                and self.row_starts.is_cuda and self.col_ids.is_cuda
+                and self.row_starts.data_ptr() % 16 == 0 and self.col_ids.data_ptr() % 16 == 0):
+            tile = [int(v) for v in os.environ.get("SB200_BS6_TILE", "0,0,0").split(",")]
+            L = _lib.lib()
+            info = _lib.Bs6Staged()
+            rc = L.sb_bs6_staged_init(*geo, *tile, info)
+            if rc == _lib.SB_OK:
+                dev = self.row_starts.device
+                plan = torch.empty(max(1, info.n_tiles * info.words_per_tile), dtype=torch.int32,
+                                   device=dev)
+                _lib.check(L.sb_bs6_staged_make_plan(info, self.row_starts.data_ptr(),
+                                                     plan.data_ptr(), _lib.stream_handle(dev)),
+                           "bs6 staged plan")
+                # consumers may run on other streams: the plan is complete once built
+                torch.cuda.current_stream(dev).synchronize()
+                st = (info, plan)
+        object.__setattr__(self, "_staged", st)
+        return st
 
 
 def build_mesh(K: int, p: int, device=None) -> MeshConnectivity:
@@ -247,8 +283,9 @@ def build_gather(mesh: MeshConnectivity, nodes_per_block: int = 512) -> GatherOp
             raise ValueError(f"nodes_per_block={nodes_per_block} is below the longest row "
                              f"({cmax} nonzeros)")
     bst = _block_starts(rs, ng, nodes_per_block)
+    geo = (mesh.K, mesh.p, 0, mesh.K, 0, mesh.K * mesh.p + 1) if mesh.structured else None
     return GatherOp(ng=ng, row_starts=rs, col_ids=ci, block_starts=bst,
-                    nodes_per_block=nodes_per_block)
+                    nodes_per_block=nodes_per_block, geometry=geo)
 
 
 def build_slab_gather(K: int, p: int, z0: int, z1: int, c_lo: int, c_hi: int,
@@ -278,7 +315,7 @@ def build_slab_gather(K: int, p: int, z0: int, z1: int, c_lo: int, c_hi: int,
     ci = ci[:nnz]  # entries of planes outside [c_lo, c_hi) are not part of this operator
     bst = _block_starts(rs, ng, nodes_per_block)
     return GatherOp(ng=ng, row_starts=rs, col_ids=ci, block_starts=bst,
-                    nodes_per_block=nodes_per_block)
+                    nodes_per_block=nodes_per_block, geometry=(K, p, z0, z1, c_lo, c_hi))
 
 
 def build_slab_l2g(K: int, p: int, z0: int, z1: int, device=None) -> torch.Tensor:
