@@ -62,7 +62,39 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--collective", choices=["nccl", "fused"], default="nccl",
+                    help="N>1: NCCL collectives (default) or the fused in-kernel NVLink combine")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch / rendezvous check only: every rank reports its pid, no GPU work")
     return ap.parse_args(argv)
+
+
+# ------------------------------------------------------------ rank launch
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args, argv) -> int:
+    """`bench.py --gpus N` outside a launcher: start N ranks with
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1) and
+    return their exit code; rank 0 prints the JSON line."""
+    backend = os.environ.get("SB200_DIST_BACKEND", "nccl")
+    if not args.dry_run and args.impl == "ours" and backend == "nccl":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have} "
+                  "(SB200_DIST_BACKEND=gloo shares one GPU between ranks for a functional check)",
+                  file=sys.stderr, flush=True)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.run(cmd, env=dict(os.environ, SB200_SELF_LAUNCHED="1")).returncode
 
 
 # ---------------------------------------------------------------- helpers
@@ -404,7 +436,7 @@ def run_e2e(args, device, steps):
     ql = torch.zeros(mesh.nl, dtype=torch.float64).pin_memory()
     nb8 = 8 * n
     h2d = {"bs1": nb8, "bs2": 2 * nb8, "bs3": nb8, "bs4": 2 * nb8, "bs5": 4 * nb8,
-           "bs6": 8 * mesh.nl, "bs7": 8 * mesh.ng + 8 * mesh.nl}
+           "bs6": 8 * mesh.nl, "bs7": 8 * mesh.ng}  # BS7: q_local is write-only (never uploaded)
     d2h = {"bs1": nb8, "bs2": nb8, "bs3": 8, "bs4": 8, "bs5": 2 * nb8 + 8, "bs6": 8 * mesh.ng,
            "bs7": 8 * mesh.nl}
     byts = {t: bytes_moved(t, n=n) for t in TESTS[:5]}
@@ -467,7 +499,7 @@ def main_ours(args):
         else:
             dist.init_process_group(backend)
         from paper_2009_10917_b200 import dist as D
-        dist_ctx = D.BenchContext(rank, world, args, device)
+        dist_ctx = D.BenchContext(rank, world, args, device, use_lsa=args.collective == "fused")
 
         def barrier():
             if backend == "nccl":
@@ -484,18 +516,29 @@ def main_ours(args):
         time.sleep(0.25)  # let the sampler flush the last interval
     iso_ms = time_isolated(w, max(3, args.steps))
     step_ms = total_ms / args.steps
+    per_rank = None
     if world > 1:
-        t = torch.tensor([step_ms] + [per_ms[k] for k in TESTS] + [iso_ms[k] for k in TESTS],
-                         dtype=torch.float64, device=device)
+        # every rank's timings (device events on its own launch stream); the
+        # step time is the max over ranks
+        mine = torch.tensor([step_ms] + [per_ms[k] for k in TESTS] + [iso_ms[k] for k in TESTS],
+                            dtype=torch.float64, device=device)
         if backend == "nccl":
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            allr = torch.empty(world, mine.numel(), dtype=torch.float64, device=device)
+            dist.all_gather_into_tensor(allr, mine)
+            allr = allr.cpu()
         else:
-            tc = t.cpu()
-            dist.all_reduce(tc, op=dist.ReduceOp.MAX)
-            t = tc
+            parts = [torch.empty(mine.numel(), dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(parts, mine.cpu())
+            allr = torch.stack(parts)
+        t = allr.max(dim=0).values
         step_ms = float(t[0])
         per_ms = {k: float(t[i + 1]) for i, k in enumerate(TESTS)}
         iso_ms = {k: float(t[len(TESTS) + i + 1]) for i, k in enumerate(TESTS)}
+        rank_bytes = sum(w.bytes.values())
+        per_rank = [{"rank": r, "ms_per_step": round(float(allr[r, 0]), 4),
+                     "GBps": round(rank_bytes / (float(allr[r, 0]) * 1e-3) / 1e9, 1),
+                     "device": f"cuda:{r % max(1, torch.cuda.device_count())}"}
+                    for r in range(world)]
     bytes_step = sum(w.bytes.values()) * world
     value = bytes_step / (step_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
@@ -536,6 +579,7 @@ def main_ours(args):
             "frac_of_peak": round(value / agg_peak, 4),
             "frac_of_nominal_8TBps": round(value / (8000.0 * world), 4),
             "per_test": per_test, "roofline": roof,
+            **({"per_rank": per_rank, "aggregate_peak_GBps": round(agg_peak, 1)} if per_rank else {}),
             "gpu_launches": w.launches_per_step * args.steps,
             "clocks": clk.summary(),
         }
@@ -582,7 +626,7 @@ def main_reference(args):
         vals.append(v)
     value = statistics.median(vals)
     out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
-           "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+           "n_gpus": int(os.environ.get("WORLD_SIZE", str(args.gpus))), "steps": args.steps,
            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded U(-1,1) fp64 (numpy)",
            "config": {"workload": f"BS1-BS5 at n={int(args.n):.0e} DOFs/GPU + BS6/BS7 on the "
@@ -596,8 +640,37 @@ def main_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def dry_run(args):
+    """Each rank: rendezvous (gloo) and report (rank, pid); rank 0 prints them."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    mine = {"rank": rank, "pid": os.getpid(), "local_rank": int(os.environ.get("LOCAL_RANK", "0"))}
+    got = [mine]
+    if world > 1:
+        dist.init_process_group("gloo")
+        got = [None] * world
+        dist.all_gather_object(got, mine)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_requested": args.gpus,
+                          "ranks": got, "self_launched": os.environ.get("SB200_SELF_LAUNCHED") == "1"}),
+              flush=True)
+
+
 def main(argv=None):
+    argv = sys.argv[1:] if argv is None else list(argv)
     args = parse_args(argv)
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        sys.exit(self_launch(args, argv))
+    if world_env is not None and int(world_env) != args.gpus and args.impl == "ours":
+        print(f"bench.py: launched with WORLD_SIZE={world_env} but --gpus {args.gpus}",
+              file=sys.stderr, flush=True)
+        sys.exit(2)
+    if args.dry_run:
+        dry_run(args)
+        return
     if args.impl == "reference":
         main_reference(args)
     else:

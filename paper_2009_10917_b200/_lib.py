@@ -9,6 +9,7 @@ caching allocator; the kernels are ours.
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 import re
 import threading
@@ -244,3 +245,38 @@ def length(a) -> int:
 
 def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
+
+
+# ---- device guard ----------------------------------------------------------
+# libsb200 launches on (and sizes grids for) the CURRENT device; torch lets a
+# caller compute on tensors of any device.  Public entry points therefore run
+# with the current device switched to their operands' device when it differs.
+
+def _cuda_index(a):
+    if isinstance(a, torch.Tensor):
+        return a.device.index if a.is_cuda else None
+    for attr in ("row_starts", "ids", "local_to_global"):  # GatherOp, ScatterIds, MeshConnectivity
+        t = getattr(a, attr, None)
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            return t.device.index
+    return None
+
+
+def device_guard(fn):
+    @functools.wraps(fn)
+    def guarded(*args, **kw):
+        for a in args:
+            d = _cuda_index(a)
+            if d is not None:
+                break
+        else:
+            d = None
+            for a in kw.values():
+                d = _cuda_index(a)
+                if d is not None:
+                    break
+        if d is None or d == torch.cuda.current_device():
+            return fn(*args, **kw)
+        with torch.cuda.device(d):
+            return fn(*args, **kw)
+    return guarded

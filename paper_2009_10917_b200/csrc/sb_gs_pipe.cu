@@ -247,6 +247,29 @@ __device__ __forceinline__ void bs6_publish_vals(const SbMeta &m, const double2 
     }
 }
 
+// A super-block beyond the kernel's capacity (more than CAP rows or entries:
+// empty rows, or a hand-built block_starts -- never from build_gather, whose
+// Python wrapper also checks) is summed straight from global memory, one
+// thread per row; callers keep the barrier so the value-tile double buffer
+// stays ordered.
+template <int T, int CAP>
+__device__ __forceinline__ bool bs6_oversize(const SbMeta &m) {
+    return m.r1 - m.r0 > CAP || m.e1 - m.e0 > CAP;
+}
+
+template <int T>
+__device__ __noinline__ void bs6_rows_direct(const SbMeta &m, const int32_t *__restrict__ rs,
+                                             const int32_t *__restrict__ ci, const double *__restrict__ q,
+                                             double *__restrict__ out, const double *__restrict__ carry,
+                                             int64_t ncarry) {
+    for (int64_t r = (int64_t)m.r0 + threadIdx.x; r < m.r1; r += T) {
+        double acc = r < ncarry ? carry[r] : 0.0;
+        const int32_t hi = __ldg(rs + r + 1);
+        for (int32_t j = __ldg(rs + r); j < hi; j++) acc = add(acc, __ldg(q + __ldg(ci + j)));
+        st_stream(out + r, acc);
+    }
+}
+
 // Pairs kernel (long rows, p <= 1): thread t owns the entry pairs (2t, 2t+1)
 // and (2t+2T, 2t+2T+1) of its super-block, gathered with one 16 B load when
 // the two columns are adjacent (the 8-entry rows of p = 1 meshes pair up
@@ -276,9 +299,14 @@ __global__ void __launch_bounds__(T, MINB) k_bs6_pairs(const int32_t *__restrict
         bs6_load_rows<T, CAP>(mc, rs, rw);             // B: its row starts
         bs6_issue_cols<T, CAP>(mn, ci, cols);          // C: indices of the next one
         const SbMeta mnn = load_meta_ps<PS>(plan, sbi + 2 * g, nsbk, nsb);
-        bs6_publish_vals<T, CAP, SWZ>(mc, v, qs[buf]);
-        __syncthreads();
-        bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
+        if (bs6_oversize<T, CAP>(mc)) {
+            __syncthreads();
+            bs6_rows_direct<T>(mc, rs, ci, q, out, carry, ncarry);
+        } else {
+            bs6_publish_vals<T, CAP, SWZ>(mc, v, qs[buf]);
+            __syncthreads();
+            bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
+        }
         buf ^= 1;  // the next iteration's barrier orders reuse of this buffer
         mc = mn;
         mn = mnn;
@@ -327,11 +355,16 @@ __global__ void __launch_bounds__(T, MINB) k_bs6_lanes(const int32_t *__restrict
         for (int j = 0; j < E; j++)
             if ((int)threadIdx.x + j * T < nne) col[j] = ld_stream(ci + mn.e0 + threadIdx.x + j * T);
         const SbMeta mnn = load_meta(plan, sbi + 2 * g, nsb);
+        if (bs6_oversize<T, CAP>(mc)) {
+            __syncthreads();
+            bs6_rows_direct<T>(mc, rs, ci, q, out, carry, ncarry);
+        } else {
 #pragma unroll
-        for (int j = 0; j < E; j++)
-            if ((int)threadIdx.x + j * T < ne) qs[buf][qslot<SWZ>(threadIdx.x + j * T)] = v[j];
-        __syncthreads();
-        bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
+            for (int j = 0; j < E; j++)
+                if ((int)threadIdx.x + j * T < ne) qs[buf][qslot<SWZ>(threadIdx.x + j * T)] = v[j];
+            __syncthreads();
+            bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
+        }
         buf ^= 1;
         mc = mn;
         mn = mnn;

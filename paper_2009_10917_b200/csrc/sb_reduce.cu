@@ -181,15 +181,20 @@ __device__ __forceinline__ void ll_put(unsigned long long *slot, double v) {
     const unsigned long long hi = (1ull << 32) | (bits >> 32), lo = (1ull << 32) | (bits & 0xffffffffull);
     asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(hi), "l"(lo) : "memory");
 }
+// Poll bound of ll_take (0 = wait forever, the default): a debug aid set from
+// SB200_POLL_LIMIT (polls; ~256 ns each after the first 4096).  A slow but
+// correct reduction -- CTAs starved by concurrent kernels, MPS partitions, a
+// sanitizer -- must not turn into a sticky launch failure.
+__device__ unsigned long long g_sb_poll_limit = 0;
+
 __device__ __forceinline__ double ll_take(unsigned long long *slot) {
     unsigned long long hi, lo;
-    for (unsigned polls = 0;; polls++) {
+    const unsigned long long limit = g_sb_poll_limit;
+    for (unsigned long long polls = 0;; polls++) {
         asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(hi), "=l"(lo) : "l"(slot) : "memory");
         if ((hi >> 32) == 1ull && (lo >> 32) == 1ull) break;
         if (polls >= 4096) __nanosleep(256);
-        // a slot that is never published is a bug: fail the launch (seconds
-        // of polling) instead of hanging the device
-        if (polls == (1u << 24)) __trap();
+        if (limit && polls == limit) __trap();
     }
     asm volatile("st.global.v2.u64 [%0], {%1, %1};" ::"l"(slot), "l"(0ull) : "memory");
     return __longlong_as_double((long long)(((hi & 0xffffffffull) << 32) | (lo & 0xffffffffull)));
@@ -534,9 +539,21 @@ static int64_t tma_min_override() {
     return v;
 }
 
+// SB200_POLL_LIMIT -> g_sb_poll_limit, once per device (max 64 devices tracked)
+static void set_poll_limit_once() {
+    static const char *e = getenv("SB200_POLL_LIMIT");
+    if (!e || !e[0]) return;
+    static unsigned long long done = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || (done >> dev) & 1ull) return;
+    const unsigned long long v = strtoull(e, nullptr, 10);
+    if (cudaMemcpyToSymbol(g_sb_poll_limit, &v, sizeof(v)) == cudaSuccess) done |= 1ull << dev;
+}
+
 template <int MODE>
 static int launch_reduce(RArgs A, void *ws, cudaStream_t st, const char *name) {
     clear_error();
+    set_poll_limit_once();
     if (A.bs < 2 || (A.bs & (A.bs - 1)) || A.nb < 1) {
         set_error("%s: block_size must be a power of two >= 2 and n_blocks >= 1 (got %lld, %lld)",
                   name, (long long)A.bs, (long long)A.nb);

@@ -381,6 +381,34 @@ class _Ids:
 
 # -------------------------------------------------------------- bench glue
 
+def _create_with_deadline(make, seconds: float, expected_exc):
+    """Run a blocking collective setup (the NCCL device-API context) with a
+    deadline: (object, None) on success, (None, why) on failure or timeout.
+    NCCL's non-blocking communicators cannot back a device communicator
+    (ncclDevCommCreate rejects them), so the setup runs in a daemon thread and
+    this rank gives up waiting after `seconds`; the caller's all-reduce of the
+    outcome then moves every rank to the NCCL-collective path together (a
+    setup stuck inside NCCL stays parked in its thread, on its own
+    communicator)."""
+    import threading
+    box = {}
+
+    def run():
+        try:
+            box["obj"] = make()
+        except expected_exc as e:  # a clean refusal (NCCL < 2.28, no peer access, ...)
+            box["why"] = str(e)
+        except Exception as e:  # noqa: BLE001 -- any setup failure means "fall back"
+            box["why"] = f"{type(e).__name__}: {e}"
+
+    th = threading.Thread(target=run, name="sb200-lsa-setup", daemon=True)
+    th.start()
+    th.join(seconds)
+    if th.is_alive():
+        return None, f"setup did not finish within {seconds:.0f} s"
+    return box.get("obj"), box.get("why")
+
+
 class BenchContext:
     """Per-rank state of bench.py's weak-scaling step (n per rank, K_g^3 mesh)."""
 
@@ -394,8 +422,8 @@ class BenchContext:
         self.lsa = None
         self.collective = ("nccl" if _nccl(None) else "gloo (host-staged)") + \
             " all_gather + sb_sum_ordered; BS6/BS7 halos by send/recv"
-        if use_lsa is None:
-            use_lsa = _nccl(None) and os.environ.get("SB200_LSA", "1") != "0"
+        if use_lsa is None:  # plain NCCL collectives unless asked for (SB200_LSA=1)
+            use_lsa = os.environ.get("SB200_LSA", "0") == "1" and _nccl(None)
         if use_lsa:
             from . import lsa as _lsa
             # first agree that every rank can even try (local checks), so no
@@ -405,10 +433,14 @@ class BenchContext:
             if world > 1:
                 dist.all_reduce(can, op=dist.ReduceOp.MIN)
             if int(can.item()) == 1:
-                try:
-                    self.lsa = _lsa.LsaReducer(world, rank, device)
+                try:  # the id broadcast stays on this thread (the group's collective order)
+                    uid = _lsa.exchange_unique_id(world, rank, device)
                 except _lsa.LsaUnavailable as e:
-                    why = str(e)
+                    uid, why = None, str(e)
+                if uid is not None:
+                    self.lsa, why = _create_with_deadline(
+                        lambda: _lsa.LsaReducer(world, rank, device, unique_id=uid),
+                        float(os.environ.get("SB200_LSA_SETUP_S", "60")), _lsa.LsaUnavailable)
             elif why is None:
                 why = "another rank cannot set it up"
             # every rank must take the same path (the fused kernels are collective)

@@ -21,6 +21,7 @@ def _dev_int(a, name, device):
     return _lib.stage(a, torch.int32, name, device).dev
 
 
+@_lib.device_guard
 def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) -> torch.Tensor:
     """Device-only BS6 writing `out` (length op.ng); optional carry-in partials
     seed rows [0, len(carry)) instead of +0.0 (multi-GPU carry halo)."""
@@ -101,6 +102,7 @@ def _bs6_host(op, q_local):
     return res.numpy() if isinstance(q_local, np.ndarray) else res
 
 
+@_lib.device_guard
 def bs6_gather(op, q_local, out=None):
     """gs.py:10-39: out[r] = sum of q_local over row r's columns, ascending order."""
     if q_local.shape[0] != op.nl:
@@ -146,6 +148,7 @@ def _bs7_host(ids, q_global, q_local) -> None:
     hoststream.run_prefix(hg, gd, ld, hl, jobs, launch, dev)
 
 
+@_lib.device_guard
 def bs7_scatter(ids, q_global, q_local) -> None:
     """gs.py:42-61: q_local[n] = q_global[ids[n]] where ids[n] >= 0; masked entries untouched."""
     if q_local.shape[0] != ids.nl:

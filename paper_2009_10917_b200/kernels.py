@@ -72,6 +72,40 @@ def _fast_vecs(*vs):
     return dev
 
 
+def _span(v):
+    """(start, end) byte range of a vector's data, or None when unknown."""
+    if isinstance(v, torch.Tensor):
+        return (v.data_ptr(), v.data_ptr() + v.numel() * v.element_size()) if v.numel() else None
+    try:
+        import numpy as np
+        a = np.asarray(v)
+        if a.size == 0:
+            return None
+        lo, hi = np.byte_bounds(a) if hasattr(np, "byte_bounds") else np.lib.array_utils.byte_bounds(a)
+        return (lo, hi)
+    except Exception:  # noqa: BLE001 -- not array-like: no aliasing to report
+        return None
+
+
+def _aliasing(outs, ins) -> str:
+    """How output vectors overlap the other arguments: "none", "same" (only
+    identical vectors: same address and length), or "partial"."""
+    kind = "none"
+    allv = list(outs) + list(ins)
+    for i, o in enumerate(outs):
+        so = _span(o)
+        if so is None:
+            continue
+        for j, v in enumerate(allv):
+            if j == i:
+                continue
+            sv = _span(v)
+            if sv is None or sv[1] <= so[0] or so[1] <= sv[0]:
+                continue
+            kind = "same" if (sv == so and kind != "partial") else "partial"
+    return kind
+
+
 def _stage_all(names, vs):
     dev = None
     for v in vs:
@@ -108,14 +142,21 @@ def _result(dev, out):
 
 # ---- BS1 -------------------------------------------------------------------
 
+@_lib.device_guard
 def bs1_copy(x, y) -> None:
-    """kernels.py:90-93: y = x (in place)."""
+    """kernels.py:90-93: y = x (in place).  Overlapping (non-identical) x and
+    y copy through a temporary, as numpy's slice assignment does."""
     dev = _fast_vecs(x, y)
     if dev is not None:
+        px, py = x.data_ptr(), y.data_ptr()
+        if px != py and abs(px - py) < 8 * x.shape[0]:
+            x = x.clone()
         _lib.check(_lib.lib().sb_bs1_copy(x.data_ptr(), y.data_ptr(), x.shape[0], _lib.stream_handle(dev)),
                    "bs1_copy")
         return
     check_same_length(x, y)
+    if _aliasing((y,), (x,)) == "partial":
+        x = x.clone() if isinstance(x, torch.Tensor) else x.copy()
     if _all_cuda(x, y):
         _check_vec(x, "x"); _check_vec(y, "y")
         dev = _same_device(x, y)
@@ -135,14 +176,22 @@ def bs1_copy(x, y) -> None:
 
 # ---- BS2 -------------------------------------------------------------------
 
+@_lib.device_guard
 def bs2_axpy(alpha: float, x, beta: float, y) -> None:
-    """kernels.py:96-103: y = alpha*x + beta*y, one rounded multiply-add pair per element."""
+    """kernels.py:96-103: y = alpha*x + beta*y, one rounded multiply-add pair per element.
+    x may be y (elementwise); partially overlapping x and y go through a copy of x
+    (the reference evaluates alpha*x into a temporary first)."""
     dev = _fast_vecs(x, y)
     if dev is not None:
+        px, py = x.data_ptr(), y.data_ptr()
+        if px != py and abs(px - py) < 8 * x.shape[0]:
+            x = x.clone()
         _lib.check(_lib.lib().sb_bs2_axpy(float(alpha), x.data_ptr(), float(beta), y.data_ptr(), x.shape[0],
                                           _lib.stream_handle(dev)), "bs2_axpy")
         return
     check_same_length(x, y)
+    if _aliasing((y,), (x,)) == "partial":
+        x = x.clone() if isinstance(x, torch.Tensor) else x.copy()
     if _all_cuda(x, y):
         _check_vec(x, "x"); _check_vec(y, "y")
         dev = _same_device(x, y)
@@ -172,6 +221,7 @@ def _cfg(cfg: ReductionConfig) -> ReductionConfig:
     return cfg
 
 
+@_lib.device_guard
 def bs3_norm2_async(x: DVector, cfg: ReductionConfig = DEFAULT_REDUCTION, out=None) -> torch.Tensor:
     """bs3_norm2 leaving the scalar on the device (no host sync)."""
     cfg = _cfg(cfg)
@@ -188,6 +238,7 @@ def bs3_norm2_async(x: DVector, cfg: ReductionConfig = DEFAULT_REDUCTION, out=No
     return res
 
 
+@_lib.device_guard
 def bs3_norm2(x, cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
     """kernels.py:106-108: sum(x[i]^2) via the fixed two-stage schedule."""
     if not _all_cuda(x):
@@ -197,6 +248,7 @@ def bs3_norm2(x, cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
     return float(bs3_norm2_async(x, cfg).item())
 
 
+@_lib.device_guard
 def bs4_dot_async(x: DVector, y: DVector, cfg: ReductionConfig = DEFAULT_REDUCTION,
                   out=None) -> torch.Tensor:
     cfg = _cfg(cfg)
@@ -214,6 +266,7 @@ def bs4_dot_async(x: DVector, y: DVector, cfg: ReductionConfig = DEFAULT_REDUCTI
     return res
 
 
+@_lib.device_guard
 def bs4_dot(x, y, cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
     """kernels.py:111-114: sum(x[i]*y[i]) via the fixed two-stage schedule."""
     check_same_length(x, y)
@@ -227,10 +280,19 @@ def bs4_dot(x, y, cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
     return float(bs4_dot_async(x, y, cfg).item())
 
 
+@_lib.device_guard
 def bs5_fused_cg_update_async(alpha: float, p: DVector, ap: DVector, x: DVector, r: DVector,
                               cfg: ReductionConfig = DEFAULT_REDUCTION, out=None) -> torch.Tensor:
     cfg = _cfg(cfg)
     dev = _fast_vecs(p, ap, x, r)
+    if dev is not None:
+        n8 = 8 * x.shape[0]
+        pp, pa, px, pr = p.data_ptr(), ap.data_ptr(), x.data_ptr(), r.data_ptr()
+        if (abs(px - pr) < n8 or abs(px - pp) < n8 or abs(px - pa) < n8 or abs(pr - pp) < n8
+                or abs(pr - pa) < n8):
+            return _bs5_sequential(alpha, p, ap, x, r, cfg, out)
+    elif _aliasing((x, r), (p, ap)) != "none":
+        return _bs5_sequential(alpha, p, ap, x, r, cfg, out)
     if dev is None:
         check_same_length(p, ap, x, r)
         for v, nm in ((p, "p"), (ap, "ap"), (x, "x"), (r, "r")):
@@ -246,13 +308,34 @@ def bs5_fused_cg_update_async(alpha: float, p: DVector, ap: DVector, x: DVector,
     return res
 
 
+def _bs5_sequential(alpha, p, ap, x, r, cfg, out=None):
+    """BS5 with aliased vectors: the reference's own order
+    (kernels.py:127-131) -- x += alpha*p over the whole vector, then
+    r -= alpha*ap, then the BS3 lattice over r -- as BS2, BS2, BS3 launches
+    (bitwise the fused kernel when nothing aliases: (-alpha)*ap + r == r - alpha*ap).
+    Only identical vectors may alias; partial overlaps are rejected."""
+    if _aliasing((x, r), (p, ap)) == "partial":
+        raise ValueError("bs5_fused_cg_update: vectors overlap without being identical")
+    check_same_length(p, ap, x, r)
+    bs2_axpy(alpha, p, 1.0, x)
+    bs2_axpy(-alpha, ap, 1.0, r)
+    if _all_cuda(r):
+        return bs3_norm2_async(r, cfg, out)
+    return torch.tensor([bs3_norm2(r, cfg)], dtype=torch.float64)
+
+
+@_lib.device_guard
 def bs5_fused_cg_update(alpha: float, p, ap, x, r,
                         cfg: ReductionConfig = DEFAULT_REDUCTION) -> float:
     """kernels.py:117-132: x += alpha*p; r -= alpha*ap; returns sum(r_new^2).
 
     Genuinely single-pass on the device (48 B/element), same lattice as BS3.
+    Aliased arguments (x is r, p is x, ...) follow the reference's sequential
+    order instead (_bs5_sequential).
     """
     check_same_length(p, ap, x, r)
+    if _aliasing((x, r), (p, ap)) != "none":
+        return float(_bs5_sequential(alpha, p, ap, x, r, _cfg(cfg)).item())
     if _all_cuda(p, ap, x, r):
         return float(bs5_fused_cg_update_async(alpha, p, ap, x, r, cfg).item())
     if hoststream.all_host(p, ap, x, r):

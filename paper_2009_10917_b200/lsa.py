@@ -51,6 +51,31 @@ def capable(world: int, device) -> str | None:
     return None
 
 
+def exchange_unique_id(world: int, rank: int, device, group=None) -> bytes:
+    """Rank 0's NCCL unique id, broadcast over the torch.distributed group.
+    An all-zero id is the "rank 0 failed" sentinel: every rank still joins
+    the broadcast and then raises, instead of waiting in it."""
+    L = _lib.lib()
+    t = torch.zeros(UID_BYTES, dtype=torch.uint8)
+    why = ""
+    if rank == 0:
+        raw = ctypes.create_string_buffer(UID_BYTES)
+        if L.sb_lsa_unique_id(raw, UID_BYTES) == _lib.SB_OK:
+            t = torch.frombuffer(bytearray(raw.raw), dtype=torch.uint8).clone()
+        else:
+            why = _lib.last_error()
+    if world > 1:
+        if dist.get_backend(group) == "nccl":
+            td = t.to(torch.device(device))
+            dist.broadcast(td, 0, group=group)
+            t = td.cpu()
+        else:
+            dist.broadcast(t, 0, group=group)
+    if not bool(t.any()):
+        raise LsaUnavailable(f"rank 0 could not create an NCCL unique id {why}".strip())
+    return bytes(t.numpy().tobytes())
+
+
 class LsaReducer:
     def __init__(self, world: int, rank: int, device, group=None, unique_id: bytes | None = None):
         self.L = _lib.lib()
@@ -67,26 +92,7 @@ class LsaReducer:
         self._ws = {}
 
     def _exchange_uid(self, group) -> bytes:
-        # an all-zero id is the "rank 0 failed" sentinel: every rank still
-        # joins the broadcast and then raises, instead of waiting in it
-        t = torch.zeros(UID_BYTES, dtype=torch.uint8)
-        why = ""
-        if self.rank == 0:
-            raw = ctypes.create_string_buffer(UID_BYTES)
-            if self.L.sb_lsa_unique_id(raw, UID_BYTES) == _lib.SB_OK:
-                t = torch.frombuffer(bytearray(raw.raw), dtype=torch.uint8).clone()
-            else:
-                why = _lib.last_error()
-        if self.world > 1:
-            if dist.get_backend(group) == "nccl":
-                td = t.to(self.device)
-                dist.broadcast(td, 0, group=group)
-                t = td.cpu()
-            else:
-                dist.broadcast(t, 0, group=group)
-        if not bool(t.any()):
-            raise LsaUnavailable(f"rank 0 could not create an NCCL unique id {why}".strip())
-        return bytes(t.numpy().tobytes())
+        return exchange_unique_id(self.world, self.rank, self.device, group)
 
     @staticmethod
     def unique_id() -> bytes:

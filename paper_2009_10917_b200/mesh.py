@@ -144,6 +144,8 @@ class GatherOp:
                 _lib.check(L.sb_bs6_make_plan(self.block_starts.data_ptr(), self.n_blocks,
                                               self.row_starts.data_ptr(), self.nodes_per_block,
                                               p.data_ptr(), _lib.stream_handle(dev)), "bs6 plan")
+                # built once per operator; consumers may run on other streams
+                torch.cuda.current_stream(dev).synchronize()
         object.__setattr__(self, "_plan", p)
         return p
 
@@ -195,10 +197,12 @@ def build_mesh(K: int, p: int, device=None) -> MeshConnectivity:
     dev = _dev(device)
     l2g = torch.empty(nl, dtype=INDEX_DTYPE, device=dev)
     L = _lib.lib()
-    _lib.check(L.sb_build_l2g(K, p, 0, K, l2g.data_ptr(), _lib.stream_handle(dev)), "build_mesh")
+    with torch.cuda.device(dev):
+        _lib.check(L.sb_build_l2g(K, p, 0, K, l2g.data_ptr(), _lib.stream_handle(dev)), "build_mesh")
     return MeshConnectivity(K=K, p=p, local_to_global=l2g, structured=True)
 
 
+@_lib.device_guard
 def build_scatter_ids(mesh: MeshConnectivity, mask=None) -> ScatterIds:
     """mesh.py:100-110: scatter id map for the mesh; global ids in `mask` become -1."""
     l2g = mesh.local_to_global
@@ -247,6 +251,7 @@ def _block_starts(row_starts: torch.Tensor, ng: int, npb: int) -> torch.Tensor:
     return bst[: nb + 1].clone()
 
 
+@_lib.device_guard
 def build_gather(mesh: MeshConnectivity, nodes_per_block: int = 512) -> GatherOp:
     """mesh.py:113-147: CSR gather operator with greedily packed row blocks.
 
@@ -329,6 +334,7 @@ def build_slab_l2g(K: int, p: int, z0: int, z1: int, device=None) -> torch.Tenso
     return l2g
 
 
+@_lib.device_guard
 def multiplicity(mesh: MeshConnectivity) -> torch.Tensor:
     """mesh.py:150-153: per-global-node count of element-local copies (float64, device)."""
     l2g = mesh.local_to_global

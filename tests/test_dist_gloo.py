@@ -162,6 +162,7 @@ def _agree_worker(rank, world, port, fail_rank, results):
                 closed.append(True)
 
         LSA.LsaReducer = FakeLsa
+        LSA.exchange_unique_id = lambda *a, **k: b"\x01" * LSA.UID_BYTES  # (no NCCL on CPU)
         LSA.capable = lambda world, device: None  # every rank passes the local checks
         ctx = D.BenchContext(rank, world, types.SimpleNamespace(K=4, order=2), "cpu", use_lsa=True)
         results[rank] = (ctx.lsa is None, "unavailable" in ctx.collective, bool(closed) or rank == fail_rank)

@@ -99,7 +99,7 @@ def test_bench_context_fused_combine_one_rank(sb):
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     try:
         args = types.SimpleNamespace(K=6, order=3)
-        ctx = D.BenchContext(0, 1, args, dev)
+        ctx = D.BenchContext(0, 1, args, dev, use_lsa=True)  # (bench default: NCCL collectives)
         assert ctx.lsa is not None, ctx.collective
         cfg = KN.ReductionConfig()
         x, y, p, ap, r = (torch.empty(2_000_003, dtype=torch.float64, device=dev).uniform_(-1, 1)
