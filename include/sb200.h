@@ -107,7 +107,11 @@ int sb_bs6_gather(const int32_t *block_starts, int64_t n_blocks, const int32_t *
  * persistent kernel keep index tiles, value gathers and row sums of three
  * super-blocks in flight.  sb_bs6_plan_size returns the number of int32
  * plan entries (0 if nodes_per_block > 512: use sb_bs6_gather);
- * sb_bs6_make_plan fills it once per operator.  row_starts and col_ids must
+ * sb_bs6_make_plan fills it once per operator and synchronises its stream
+ * once: the plan's trailer word flags a super-block with more than 512 rows
+ * or entries (empty rows or a hand-built block_starts), and such a plan is
+ * remembered by address so sb_bs6_gather_planned sums its rows straight from
+ * global memory (still bitwise).  row_starts and col_ids must
  * be 16-byte aligned.  Results are bitwise those of sb_bs6_gather. */
 int64_t sb_bs6_plan_size(int64_t n_blocks, int64_t nodes_per_block);
 int sb_bs6_make_plan(const int32_t *block_starts, int64_t n_blocks, const int32_t *row_starts,
@@ -147,6 +151,26 @@ int sb_bs6_gather_staged(const sb_bs6_staged_t *info, const int32_t *plan,
                          const int32_t *row_starts, const int32_t *col_ids, int64_t ng, int64_t nl,
                          const double *q_local, double *out, const double *carry_in,
                          int64_t n_carry, sb_stream_t stream);
+
+/* z-sweep BS6 for structured operators of order p <= 2 (the fast path
+ * there; csrc/sb_gs_sweep.cu).  The operator's rows must be the lattice rows
+ * of planes [c_lo, c_hi) of the slab z0..z1 of a K^3 order-p build_mesh
+ * numbering (the sb_build_gather_csr geometry; whole mesh: 0, K, 0, K*p+1),
+ * so ng = (c_hi-c_lo)*(K*p+1)^2 and nl = K*K*(z1-z0)*(p+1)^3.  A persistent
+ * kernel sweeps columns of 32 x 8 rows along z, staging each element plane
+ * under a column in shared memory once (cp.async.bulk) and reading the
+ * entries from there.  Columns outside the staged element runs are read from
+ * global memory, so ANY CSR with these rows gives the right answer: results
+ * are bitwise those of sb_bs6_gather.  No plan; q_local 16-byte aligned. */
+int sb_bs6_gather_sweep(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_lo, int32_t c_hi,
+                        const int32_t *row_starts, const int32_t *col_ids, int64_t ng, int64_t nl,
+                        const double *q_local, double *out, const double *carry_in, int64_t n_carry,
+                        sb_stream_t stream);
+/* Process-wide knobs of sb_bs6_gather_sweep for A/B runs (not thread-safe;
+ * 0 / -1 restore the measured defaults): shared-memory ring slots (3..8,
+ * default 4), L2 prefetch distance in element planes (-1: 4; 0: off), work
+ * items per resident CTA (default 8), value-tile swizzle (-1: for p = 1). */
+int sb_bs6_sweep_tune(int32_t slots, int32_t l2_prefetch_planes, int32_t waves, int32_t swizzle);
 
 /* gs.py:42-61 bs7_scatter(ids, q_global, q_local): q_local[n] =
  * q_global[ids[n]] where ids[n] >= 0 (masked entries untouched).  The caller

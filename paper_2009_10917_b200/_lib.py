@@ -102,6 +102,9 @@ _SIGS = {
     "sb_bs6_staged_make_plan": (_c_int, [_c_st, _c_vp, _c_vp, _c_vp]),
     "sb_bs6_gather_staged": (_c_int, [_c_st, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp,
                                       _c_i64, _c_vp]),
+    "sb_bs6_gather_sweep": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_vp, _c_vp, _c_i64,
+                                     _c_i64, _c_vp, _c_vp, _c_vp, _c_i64, _c_vp]),
+    "sb_bs6_sweep_tune": (_c_int, [_c_int, _c_int, _c_int, _c_int]),
     "sb_bs6_make_plan": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_vp]),
     "sb_bs6_gather_planned": (_c_int, [_c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp,
                                        _c_vp, _c_vp, _c_i64, _c_vp]),

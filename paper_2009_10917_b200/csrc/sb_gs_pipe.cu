@@ -26,6 +26,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 
 #include "sb_common.cuh"
 
@@ -95,14 +97,26 @@ int bs7_lanes_launch(const int32_t *ids, int64_t nl, const double *qg, double *q
 // plan[2i] = first row of super-block i, plan[2i+1] = its first entry;
 // super-block i = operator blocks [i*G, (i+1)*G), G = max(1, CAP/npb), so a
 // super-block has <= CAP entries and <= CAP rows (rows are non-empty).
+// plan[2 (nsb+1)] (the trailer word, zeroed by the host first) is set when a
+// super-block holds more than CAP rows or entries (empty rows, or a
+// hand-built block_starts -- never from build_gather).  sb_bs6_make_plan reads
+// it back once and records the plan as oversize; sb_bs6_gather_planned then
+// sums its rows straight from global memory (bs6_rows_launch).  (A check
+// inside the kernels cost 2-10% even at entry: profiles/r02_bs6_sweep.md.)
 __global__ void k_bs6_plan(const int32_t *bst, int64_t nblk, const int32_t *rs, int G, int64_t nsb,
                            int32_t *plan) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nsb;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = i * G < nblk ? i * G : nblk;
         const int32_t r = bst[b];
+        const int32_t e = rs[r];
         plan[2 * i] = r;
-        plan[2 * i + 1] = rs[r];
+        plan[2 * i + 1] = e;
+        if (i < nsb) {
+            const int64_t bn = (i + 1) * G < nblk ? (i + 1) * G : nblk;
+            const int32_t rn = bst[bn];
+            if ((int64_t)rn - r > kBs6Cap || (int64_t)rs[rn] - e > kBs6Cap) atomicOr(plan + 2 * (nsb + 1), 1);
+        }
     }
 }
 
@@ -247,29 +261,6 @@ __device__ __forceinline__ void bs6_publish_vals(const SbMeta &m, const double2 
     }
 }
 
-// A super-block beyond the kernel's capacity (more than CAP rows or entries:
-// empty rows, or a hand-built block_starts -- never from build_gather, whose
-// Python wrapper also checks) is summed straight from global memory, one
-// thread per row; callers keep the barrier so the value-tile double buffer
-// stays ordered.
-template <int T, int CAP>
-__device__ __forceinline__ bool bs6_oversize(const SbMeta &m) {
-    return m.r1 - m.r0 > CAP || m.e1 - m.e0 > CAP;
-}
-
-template <int T>
-__device__ __noinline__ void bs6_rows_direct(const SbMeta &m, const int32_t *__restrict__ rs,
-                                             const int32_t *__restrict__ ci, const double *__restrict__ q,
-                                             double *__restrict__ out, const double *__restrict__ carry,
-                                             int64_t ncarry) {
-    for (int64_t r = (int64_t)m.r0 + threadIdx.x; r < m.r1; r += T) {
-        double acc = r < ncarry ? carry[r] : 0.0;
-        const int32_t hi = __ldg(rs + r + 1);
-        for (int32_t j = __ldg(rs + r); j < hi; j++) acc = add(acc, __ldg(q + __ldg(ci + j)));
-        st_stream(out + r, acc);
-    }
-}
-
 // Pairs kernel (long rows, p <= 1): thread t owns the entry pairs (2t, 2t+1)
 // and (2t+2T, 2t+2T+1) of its super-block, gathered with one 16 B load when
 // the two columns are adjacent (the 8-entry rows of p = 1 meshes pair up
@@ -299,14 +290,9 @@ __global__ void __launch_bounds__(T, MINB) k_bs6_pairs(const int32_t *__restrict
         bs6_load_rows<T, CAP>(mc, rs, rw);             // B: its row starts
         bs6_issue_cols<T, CAP>(mn, ci, cols);          // C: indices of the next one
         const SbMeta mnn = load_meta_ps<PS>(plan, sbi + 2 * g, nsbk, nsb);
-        if (bs6_oversize<T, CAP>(mc)) {
-            __syncthreads();
-            bs6_rows_direct<T>(mc, rs, ci, q, out, carry, ncarry);
-        } else {
-            bs6_publish_vals<T, CAP, SWZ>(mc, v, qs[buf]);
-            __syncthreads();
-            bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
-        }
+        bs6_publish_vals<T, CAP, SWZ>(mc, v, qs[buf]);
+        __syncthreads();
+        bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
         buf ^= 1;  // the next iteration's barrier orders reuse of this buffer
         mc = mn;
         mn = mnn;
@@ -355,16 +341,11 @@ __global__ void __launch_bounds__(T, MINB) k_bs6_lanes(const int32_t *__restrict
         for (int j = 0; j < E; j++)
             if ((int)threadIdx.x + j * T < nne) col[j] = ld_stream(ci + mn.e0 + threadIdx.x + j * T);
         const SbMeta mnn = load_meta(plan, sbi + 2 * g, nsb);
-        if (bs6_oversize<T, CAP>(mc)) {
-            __syncthreads();
-            bs6_rows_direct<T>(mc, rs, ci, q, out, carry, ncarry);
-        } else {
 #pragma unroll
-            for (int j = 0; j < E; j++)
-                if ((int)threadIdx.x + j * T < ne) qs[buf][qslot<SWZ>(threadIdx.x + j * T)] = v[j];
-            __syncthreads();
-            bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
-        }
+        for (int j = 0; j < E; j++)
+            if ((int)threadIdx.x + j * T < ne) qs[buf][qslot<SWZ>(threadIdx.x + j * T)] = v[j];
+        __syncthreads();
+        bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], out, carry, ncarry);
         buf ^= 1;
         mc = mn;
         mn = mnn;
@@ -376,6 +357,11 @@ int bs6_rows_launch(const int32_t *rs, const int32_t *ci, int64_t ng, const doub
 
 static int64_t bs6_G(int64_t npb) { return std::max<int64_t>(1, kBs6Cap / npb); }
 
+// plans sb_bs6_make_plan found oversize (keyed by the plan's address; a new
+// plan built at the same address overwrites its entry)
+static std::mutex g_plan_mu;
+static std::unordered_map<const int32_t *, bool> g_plan_oversize;
+
 }  // namespace sb
 
 using namespace sb;
@@ -385,7 +371,7 @@ extern "C" {
 int64_t sb_bs6_plan_size(int64_t n_blocks, int64_t npb) {
     if (n_blocks < 1 || npb < 1 || npb > kBs6Cap) return 0;
     const int64_t G = bs6_G(npb);
-    return 2 * ((n_blocks + G - 1) / G + 1);
+    return 2 * ((n_blocks + G - 1) / G + 1) + 2;  // + the oversize trailer (and its pad)
 }
 
 int sb_bs6_make_plan(const int32_t *bst, int64_t nblk, const int32_t *rs, int64_t npb, int32_t *plan,
@@ -398,8 +384,21 @@ int sb_bs6_make_plan(const int32_t *bst, int64_t nblk, const int32_t *rs, int64_
     const int G = (int)bs6_G(npb);
     const int64_t nsb = (nblk + G - 1) / G;
     const int64_t grid = std::min<int64_t>((nsb + 256) / 256, (int64_t)sm_count() * 16);
+    int rc = cuda_check(cudaMemsetAsync(plan + 2 * (nsb + 1), 0, 2 * sizeof(int32_t), as_stream(s)),
+                        "sb_bs6_make_plan");
+    if (rc) return rc;
     k_bs6_plan<<<(unsigned)std::max<int64_t>(1, grid), 256, 0, as_stream(s)>>>(bst, nblk, rs, G, nsb, plan);
-    return launch_check("sb_bs6_make_plan");
+    rc = launch_check("sb_bs6_make_plan");
+    if (rc) return rc;
+    // one-time readback of the trailer (a plan is built once per operator)
+    int32_t flag = 0;
+    rc = cuda_check(cudaMemcpyAsync(&flag, plan + 2 * (nsb + 1), sizeof(flag), cudaMemcpyDeviceToHost, as_stream(s)),
+                    "sb_bs6_make_plan");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(as_stream(s)), "sb_bs6_make_plan");
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    g_plan_oversize[plan] = flag != 0;
+    return SB_OK;
 }
 
 int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const int32_t *rs,
@@ -418,7 +417,12 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     }
     if (ng == 0) return SB_OK;
     if (ncarry > ng) ncarry = ng;
-    const int64_t nsb = psize / 2 - 1;
+    const int64_t nsb = psize / 2 - 2;
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        const auto f = g_plan_oversize.find(plan);
+        if (f != g_plan_oversize.end() && f->second) return bs6_rows_launch(rs, ci, ng, q, out, carry, ncarry, as_stream(s));
+    }
     constexpr int T = kBs6T;
     const size_t smem = 2 * kBs6Cap * sizeof(double);
     using KernT = void (*)(const int32_t *, int64_t, const int32_t *, const int32_t *, const double *, double *,
@@ -445,7 +449,7 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     else if (nl >= 3 * ng) { pairs = false; sw = false; mb = 12; }
     else if (5 * nl >= 11 * ng) { pairs = false; sw = true; mb = 8; }
     else { pairs = false; sw = false; mb = 10; }
-    static const char *cfg = getenv("SB200_BS6_CFG");
+    const char *cfg = getenv("SB200_BS6_CFG");  // (per call: A/B runs and tests switch it)
     if (cfg && cfg[0] == 'r' && cfg[1] == 'o' && cfg[2] == 'w' && cfg[3] == 's')
         return bs6_rows_launch(rs, ci, ng, q, out, carry, ncarry, as_stream(s));
     if (cfg) {

@@ -1,0 +1,540 @@
+// sb_gs_sweep.cu -- BS6 gather for low polynomial orders (p <= 2) as a sweep
+// along z over element planes staged in shared memory (gs.py:10-39; bitwise
+// the reference: each row is summed in ascending column order from +0.0, or
+// from the carry-in, by one thread).
+//
+// Why.  At p = 1 a row's 8 entries come from 8 different elements, so every
+// 32-entry warp gather of the LSU kernels (sb_gs_pipe.cu) touches ~14
+// distinct 128 B lines and the L1 tag / data pipe, not HBM, sets the speed
+// (ncu at N=1: l1tex 84%, DRAM 59%).  Staging q in shared memory turns the
+// gathers into shared-memory reads (2 wavefronts per warp instruction at
+// p = 1: the four element runs a row line reads are bank-disjoint), but it
+// only pays if the staging stays close to one read of q: the r02 tile kernel
+// (sb_gs_staged.cu) re-read every element run for each 2x2 patch of row lines
+// (1.75x the algorithmic bytes through L2) and topped out at 2.9 TB/s.
+//
+// Here a CTA owns a column of rows -- W = 32 rows along x times H row lines
+// along y -- and sweeps it along z.  Element plane ez (the nx x ny elements
+// under the column: one contiguous run of q_local per ey) is copied into a
+// ring slot ONCE by the producer thread (cp.async.bulk, mbarrier transaction
+// count) and serves every row plane c it touches (p+1 of them); the only
+// re-read is the one-element halo a column shares with its x / y neighbours
+// ((W+1)(H+1)/(W H) ~ 1.16x of q at p = 1, H = 8), which the neighbouring
+// CTAs of the same wave load at about the same time (L2 hits).  The producer
+// also prefetches planes further ahead into L2 (cp.async.bulk.prefetch.L2)
+// so the bytes in flight are not bounded by the ring.
+//
+// Consumer warp w takes row line b = b0 + w of every row plane c: lane = row
+// for the row starts and the sums, lane = entry for the column loads (one
+// coalesced 128 B line per 32 entries), software-pipelined: column indices
+// one step ahead, row starts two steps ahead.  Each entry's column is matched
+// against the <= 4 element runs (ey, ez) its row line can touch; a column
+// outside them (an operator that is not the structured one) is read from
+// global memory, so the result is right for ANY CSR with these rows -- the
+// geometry only decides the speed.  A warp-step with more than 256 entries
+// sums its rows straight from global memory.
+#include <limits.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "sb_common.cuh"
+
+namespace sb {
+
+namespace {
+
+constexpr int kSwW = 32;    // rows along x per column (lane = row)
+constexpr int kSwVt = 256;  // value-tile entries per warp-step
+constexpr int kSwMaxSlots = 8;
+constexpr int kSwHdr = 256;  // bytes of mbarriers before the ring
+
+struct SwGeom {
+    int K, z0, z1, c_lo, c_hi, g;
+    int na, nb;       // columns along x (W rows) and y (H row lines)
+    int ch;           // row planes per item (z chunk)
+    int64_t n_items;  // na * nb * ceil((c_hi - c_lo) / ch)
+    int nslot;        // ring slots (element planes)
+    int rs_d;         // run stride in doubles (multiple of 16: runs start on bank 0)
+    int plane_d;      // slot stride in doubles
+    int pfd;          // L2 prefetch distance in planes (0: off)
+    int64_t nl;
+};
+
+// element range of lattice coordinate x (0 .. K*p) along one axis
+template <int P>
+__device__ __forceinline__ int el_lo(int x, int K) {
+    const int e = (x % P == 0 && x > 0) ? x / P - 1 : x / P;
+    return e < K - 1 ? e : K - 1;
+}
+template <int P>
+__device__ __forceinline__ int el_hi(int x, int K) {
+    const int e = x / P;
+    return e < K - 1 ? e : K - 1;
+}
+
+template <bool SWZ>
+__device__ __forceinline__ int vslot(int k) {
+    return SWZ ? (k ^ ((k >> 4) & 15)) : k;
+}
+
+// One work item: the column (ta, tb) over the row planes [c0, c1) and the
+// element planes [zf, zf + np) (global ez; slab-local numbering on use).
+struct SwItem {
+    int a0, a1, b0, c0, c1;
+    int xlo, nx, ylo, ny, zf, np;
+};
+
+template <int P, int H>
+__device__ __forceinline__ SwItem sw_item(const SwGeom &G, int64_t it) {
+    SwItem I;
+    const int ta = (int)(it % G.na);
+    const int tb = (int)((it / G.na) % G.nb);
+    const int tc = (int)(it / ((int64_t)G.na * G.nb));
+    I.a0 = ta * kSwW;
+    I.a1 = min(G.g, I.a0 + kSwW);
+    I.b0 = tb * H;
+    const int b1 = min(G.g, I.b0 + H);
+    I.c0 = G.c_lo + tc * G.ch;
+    I.c1 = min(G.c_hi, I.c0 + G.ch);
+    I.xlo = el_lo<P>(I.a0, G.K);
+    I.nx = el_hi<P>(I.a1 - 1, G.K) - I.xlo + 1;
+    I.ylo = el_lo<P>(I.b0, G.K);
+    I.ny = el_hi<P>(b1 - 1, G.K) - I.ylo + 1;
+    I.zf = max(el_lo<P>(I.c0, G.K), G.z0);
+    const int zl = min(el_hi<P>(I.c1 - 1, G.K), G.z1 - 1);
+    I.np = zl >= I.zf ? zl - I.zf + 1 : 0;
+    return I;
+}
+
+// q_local column of node 0 of element (ex, ey, ez) (slab-local numbering)
+template <int P>
+__device__ __forceinline__ int64_t sw_col(const SwGeom &G, int ex, int ey, int ez) {
+    constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
+    return ((((int64_t)(ez - G.z0) * G.K + ey) * G.K) + ex) * N3;
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_plain(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Row geometry of warp w at one (item, c) step, for the look-ahead loads.
+struct SwRows {
+    int64_t r0;
+    int n;  // rows (0: the row line lies past the mesh, or no step)
+};
+
+template <int P, int H>
+struct SwCursor {
+    int64_t it;
+    int c, c1, a0, a1, b;
+    __device__ __forceinline__ void set(const SwGeom &G, int64_t item, int w) {
+        it = item;
+        if (it < G.n_items) {
+            const int ta = (int)(it % G.na);
+            const int tb = (int)((it / G.na) % G.nb);
+            const int tc = (int)(it / ((int64_t)G.na * G.nb));
+            a0 = ta * kSwW;
+            a1 = min(G.g, a0 + kSwW);
+            b = tb * H + w;
+            c = G.c_lo + tc * G.ch;
+            c1 = min(G.c_hi, c + G.ch);
+        }
+    }
+    __device__ __forceinline__ void next(const SwGeom &G, int w) {
+        if (it >= G.n_items) return;
+        if (++c >= c1) set(G, it + gridDim.x, w);
+    }
+    __device__ __forceinline__ SwRows rows(const SwGeom &G) const {
+        SwRows R{0, 0};
+        if (it < G.n_items && b < G.g) {
+            R.r0 = ((int64_t)(c - G.c_lo) * G.g + b) * G.g + a0;
+            R.n = a1 - a0;
+        }
+        return R;
+    }
+};
+
+// lane l < n: row start of row r0 + l; every lane: the end of the last row
+__device__ __forceinline__ void sw_load_rs(const SwRows &R, const int32_t *__restrict__ rs, int lane, int &lo,
+                                           int &end) {
+    if (R.n > 0) {
+        // lanes >= n load the end too (same address): no select on a load result
+        end = __ldg(rs + R.r0 + R.n);
+        lo = ld_stream(rs + R.r0 + (lane < R.n ? lane : R.n));
+    } else {
+        lo = end = 0;
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void sw_load_cols(int lo, int end, const int32_t *__restrict__ ci, int lane,
+                                             int (&col)[E]) {
+    const int e0 = __shfl_sync(0xffffffffu, lo, 0);
+    const int ne = end - e0;
+#pragma unroll
+    for (int j = 0; j < E; j++)
+        if (lane + 32 * j < ne) col[j] = ld_stream(ci + e0 + lane + 32 * j);
+}
+
+// Consumer state of one warp: the current item / row plane and the plane
+// sequence numbers it has waited for and released.
+template <int P, int H>
+struct SwState {
+    SwItem I;
+    int64_t it;
+    int c;
+    int base;            // sequence number of the item's first plane
+    int waited, wslot;   // planes waited for (count), next slot to wait on
+    uint32_t wph;        // its phase
+    int released, rslot; // planes released (count), next slot to release
+};
+
+// One step (row plane c of the current item) of consumer warp `warp`.  colA /
+// loA / endA hold this step's column indices (loaded one step ago) and row
+// starts (two steps ago); colB is filled for the next step from loB / endB
+// (loaded one step ago), and loA / endA are refilled for the step after that
+// -- the two register sets alternate between calls, so no load result is
+// moved (and waited for) before the step that uses it.  Returns false after
+// the CTA's last step.
+template <int P, int H, bool SWZ, int E>
+__device__ __forceinline__ bool sw_step(const SwGeom &G, SwState<P, H> &S, SwCursor<P, H> &ahead, int warp,
+                                        int lane, int (&colA)[E], int (&colB)[E], int &loA, int &endA, int &loB,
+                                        int &endB, const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
+                                        const double *__restrict__ q, double *__restrict__ out,
+                                        const double *__restrict__ carry, int64_t ncarry, uint64_t *full,
+                                        uint64_t *empty, const double *ring, double *vt) {
+    const int lo0 = loA, end0 = endA;
+    sw_load_rs(ahead.rows(G), rs, lane, loA, endA);  // step + 2
+    ahead.next(G, warp);
+    sw_load_cols<E>(loB, endB, ci, lane, colB);  // step + 1
+
+    const SwItem &I = S.I;
+    const int c = S.c;
+    const int nslot = G.nslot;
+    // element planes of this row plane: wait for the newest
+    const int zlo = max(el_lo<P>(c, G.K), G.z0), zhi = min(el_hi<P>(c, G.K), G.z1 - 1);
+    if (zhi >= zlo) {
+        const int need = S.base + (zhi - I.zf) + 1;
+        for (; S.waited < need; S.waited++) {
+            mbar_wait(&full[S.wslot], S.wph);
+            if (++S.wslot == nslot) {
+                S.wslot = 0;
+                S.wph ^= 1u;
+            }
+        }
+    }
+    const int bb = I.b0 + warp;
+    if (bb < G.g) {
+        const int64_t r0 = ((int64_t)(c - G.c_lo) * G.g + bb) * G.g + I.a0;
+        const int nrows = I.a1 - I.a0;
+        const int e0 = __shfl_sync(0xffffffffu, lo0, 0);
+        const int ne = end0 - e0;
+        int nxt = __shfl_down_sync(0xffffffffu, lo0, 1);
+        if (lane == nrows - 1) nxt = end0;
+        double acc = 0.0;
+        const int64_t r = r0 + lane;
+        if (lane < nrows && r < ncarry) acc = carry[r];
+        if (ne <= kSwVt) {
+            // the <= 4 element runs (ey, ez) of this row line, ascending
+            // columns; a missing run gets cb = INT_MAX (never selected)
+            constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
+            const int ylo = el_lo<P>(bb, G.K), yhi = el_hi<P>(bb, G.K);
+            const int ystride = G.K * N3, zstride = G.K * ystride, len = I.nx * N3;
+            const bool zone = zhi >= zlo, y2 = yhi > ylo, z2 = zhi > zlo;
+            const int c00 = zone ? ((zlo - G.z0) * G.K + ylo) * ystride + I.xlo * N3 : 0;
+            int sl1 = S.rslot + 1;  // planes from zlo on are the unreleased ones: zlo is at rslot
+            if (sl1 == nslot) sl1 = 0;
+            const int s0 = S.rslot * G.plane_d + (ylo - I.ylo) * G.rs_d, s2 = sl1 * G.plane_d + (ylo - I.ylo) * G.rs_d;
+            int cb[4], dd[4];
+            cb[0] = zone ? c00 : INT_MAX;
+            cb[1] = zone && y2 ? c00 + ystride : INT_MAX;
+            cb[2] = z2 ? c00 + zstride : INT_MAX;
+            cb[3] = z2 && y2 ? c00 + zstride + ystride : INT_MAX;
+            dd[0] = s0 + (cb[0] & 1) - cb[0];
+            dd[1] = s0 + G.rs_d + (cb[1] & 1) - cb[1];
+            dd[2] = s2 + (cb[2] & 1) - cb[2];
+            dd[3] = s2 + G.rs_d + (cb[3] & 1) - cb[3];
+            // branch-free except for columns outside the runs (a warp vote)
+#pragma unroll
+            for (int j = 0; j < E; j++) {
+                const int k = lane + 32 * j;
+                const int col = colA[j];
+                int csel = cb[0], dsel = dd[0];
+#pragma unroll
+                for (int t = 1; t < 4; t++) {
+                    const bool ge = col >= cb[t];
+                    csel = ge ? cb[t] : csel;
+                    dsel = ge ? dd[t] : dsel;
+                }
+                const bool live = k < ne;
+                const bool inrun = live && (unsigned)(col - csel) < (unsigned)len;
+                double v = ring[inrun ? col + dsel : 0];
+                if (__any_sync(0xffffffffu, live && !inrun)) {
+                    if (live && !inrun) v = __ldg(q + col);  // a column outside the staged runs
+                }
+                if (live) vt[vslot<SWZ>(k)] = v;
+            }
+            __syncwarp();
+            {
+                // lanes >= nrows run the same (select-guarded) code on t0 = 0
+                const int t0 = lane < nrows ? lo0 - e0 : 0, n = lane < nrows ? nxt - lo0 : 0;
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    const double v = vt[vslot<SWZ>((t0 + t) & (kSwVt - 1))];
+                    const double sum = add(acc, v);
+                    acc = t < n ? sum : acc;
+                }
+                if (__any_sync(0xffffffffu, n > 8)) {
+#pragma unroll 1
+                    for (int t = 8; t < n; t++) acc = add(acc, vt[vslot<SWZ>(t0 + t)]);
+                }
+                if (lane < nrows) st_stream(out + r, acc);
+            }
+            __syncwarp();
+        } else if (lane < nrows) {  // long rows: straight from global memory
+#pragma unroll 1
+            for (int t = lo0; t < nxt; t++) acc = add(acc, __ldg(q + __ldg(ci + t)));
+            st_stream(out + r, acc);
+        }
+    }
+
+    // release the planes no later step of this item reads; advance
+    const int keep = (c + 1 < I.c1) ? S.base + min(max(el_lo<P>(c + 1, G.K), G.z0) - I.zf, I.np)
+                                    : S.base + I.np;
+    if (keep > S.released) {
+        __syncwarp();
+        for (; S.released < keep; S.released++) {
+            if (lane == 0) mbar_arrive(&empty[S.rslot]);
+            if (++S.rslot == nslot) S.rslot = 0;
+        }
+    }
+    if (++S.c >= I.c1) {
+        S.base += I.np;
+        S.it += gridDim.x;
+        if (S.it >= G.n_items) return false;
+        S.I = sw_item<P, H>(G, S.it);
+        S.c = S.I.c0;
+    }
+    return true;
+}
+
+template <int P, int H, bool SWZ>
+__global__ void __launch_bounds__((H + 1) * 32, 2)
+    k_bs6_sweep(SwGeom G, const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
+                const double *__restrict__ q, double *__restrict__ out, const double *__restrict__ carry,
+                int64_t ncarry) {
+    constexpr int E = kSwVt / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *empty = full + kSwMaxSlots;
+    double *ring = reinterpret_cast<double *>(smem + kSwHdr);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nslot = G.nslot;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nslot; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], H);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t grid = gridDim.x;
+
+    if (warp == H) {
+        // ------------------------------------------------ producer warp
+        // lane y < ny copies run y of each element plane; the item geometry
+        // is computed once per item, a plane is an address increment
+        constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
+        const int64_t pstride = (int64_t)G.K * G.K * N3;  // one element plane of q_local
+        const int64_t qlim = G.nl & ~int64_t(1);          // bulk copies move whole 16 B units
+        int64_t pit = blockIdx.x;                           // L2 prefetch cursor
+        SwItem PI{};
+        int pj = 0, pseq = 0;
+        bool pok = false;
+        auto p_load = [&]() {
+            for (; pit < G.n_items; pit += grid) {
+                PI = sw_item<P, H>(G, pit);
+                if (PI.np > 0) {
+                    pok = true;
+                    return;
+                }
+            }
+            pok = false;
+        };
+        if (G.pfd > 0) p_load();
+        int seq = 0, slot = 0;
+        uint32_t eph = 0;
+        for (int64_t it = blockIdx.x; it < G.n_items; it += grid) {
+            const SwItem I = sw_item<P, H>(G, it);
+            const int64_t len = (int64_t)I.nx * N3;
+            int64_t cb = lane < I.ny ? sw_col<P>(G, I.xlo, I.ylo + lane, I.zf) : 0;
+            for (int j = 0; j < I.np; j++, seq++, cb += pstride) {
+                while (pok && pseq <= seq + G.pfd) {
+                    if (pseq > seq && lane < PI.ny) {
+                        const int64_t pc = sw_col<P>(G, PI.xlo, PI.ylo + lane, PI.zf + pj);
+                        const int64_t pa = pc & ~int64_t(1), pe = min((pc + (int64_t)PI.nx * N3 + 1) & ~int64_t(1), qlim);
+                        if (pe > pa) bulk_prefetch_l2(q + pa, (uint32_t)(pe - pa) * 8u);
+                    }
+                    pseq++;
+                    if (++pj >= PI.np) {
+                        pj = 0;
+                        pit += grid;
+                        p_load();
+                    }
+                }
+                if (seq >= nslot) mbar_wait(&empty[slot], eph);
+                double *dst = ring + (size_t)slot * G.plane_d + (size_t)lane * G.rs_d;
+                const int64_t qa = cb & ~int64_t(1), qe = (cb + len + 1) & ~int64_t(1);
+                const int64_t ce = qe < qlim ? qe : qlim;
+                uint32_t bytes = 0;
+                if (lane < I.ny) {
+                    // the odd tail past the last 16 B unit of q_local: plain
+                    // stores, ordered before lane 0's arrive by the warp sync
+                    if (qe > qlim)
+                        for (int64_t x = qlim > qa ? qlim : qa; x < cb + len; x++) dst[x - qa] = __ldg(q + x);
+                    if (ce > qa) bytes = (uint32_t)(ce - qa) * 8u;
+                }
+                const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
+                if (lane == 0) mbar_arrive_expect_tx(&full[slot], total);
+                __syncwarp();
+                if (bytes) bulk_g2s_plain(dst, q + qa, bytes, &full[slot]);
+                if (++slot == nslot) {
+                    slot = 0;
+                    if (seq >= nslot) eph ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------ consumers
+    double *vt = ring + (size_t)nslot * G.plane_d + (size_t)warp * kSwVt;
+    if ((int64_t)blockIdx.x >= G.n_items) return;
+    SwState<P, H> S;
+    S.it = blockIdx.x;
+    S.I = sw_item<P, H>(G, S.it);
+    S.c = S.I.c0;
+    S.base = S.waited = S.wslot = S.released = S.rslot = 0;
+    S.wph = 0;
+    SwCursor<P, H> ahead;  // two steps ahead of S
+    ahead.set(G, S.it, warp);
+    int lo0, end0, lo1, end1;
+    sw_load_rs(ahead.rows(G), rs, lane, lo0, end0);
+    ahead.next(G, warp);
+    sw_load_rs(ahead.rows(G), rs, lane, lo1, end1);
+    ahead.next(G, warp);
+    int col0[E], col1[E];
+    sw_load_cols<E>(lo0, end0, ci, lane, col0);
+    while (sw_step<P, H, SWZ, E>(G, S, ahead, warp, lane, col0, col1, lo0, end0, lo1, end1, rs, ci, q, out,
+                                 carry, ncarry, full, empty, ring, vt) &&
+           sw_step<P, H, SWZ, E>(G, S, ahead, warp, lane, col1, col0, lo1, end1, lo0, end0, rs, ci, q, out,
+                                 carry, ncarry, full, empty, ring, vt)) {
+    }
+}
+
+constexpr int kSwH = 8;
+
+// tuning knobs (sb_bs6_sweep_tune; A/B runs and tests): <= 0 / < 0 = default
+int g_sw_slots = 0, g_sw_pfd = -1, g_sw_waves = 0, g_sw_swz = -1;
+
+template <int P>
+int sweep_launch(const SwGeom &G0, const int32_t *rs, const int32_t *ci, const double *q, double *out,
+                 const double *carry, int64_t ncarry, bool swz, cudaStream_t st) {
+    constexpr int H = kSwH;
+    SwGeom G = G0;
+    constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
+    const int nx_max = (kSwW - 1) / P + 2, ny_max = (H - 1) / P + 2;
+    G.rs_d = (nx_max * N3 + 2 + 15) / 16 * 16;  // + the odd-start shift and 16 B rounding
+    G.plane_d = ny_max * G.rs_d;
+    const size_t smem = kSwHdr + (size_t)G.nslot * G.plane_d * 8 + (size_t)H * kSwVt * 8;
+    using KernT = void (*)(SwGeom, const int32_t *, const int32_t *, const double *, double *, const double *,
+                           int64_t);
+    const KernT k = swz ? k_bs6_sweep<P, H, true> : k_bs6_sweep<P, H, false>;
+    int rc = cuda_check(cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "sb_bs6_gather_sweep: shared memory");
+    if (rc) return rc;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k, (H + 1) * 32, smem);
+    per_sm = std::max(1, per_sm);
+    const int64_t grid_max = (int64_t)sm_count() * per_sm;
+    // z chunks: about 8 items per resident CTA (tail balance) without cutting
+    // the sweep shorter than needed (each chunk re-reads one element plane)
+    const int64_t ncols = (int64_t)G.na * G.nb, nc = G.c_hi - G.c_lo;
+    const int64_t want = grid_max * (g_sw_waves > 0 ? g_sw_waves : 8);
+    int64_t nch = std::max<int64_t>(1, std::min<int64_t>(nc, (want + ncols - 1) / ncols));
+    G.ch = (int)((nc + nch - 1) / nch);
+    nch = (nc + G.ch - 1) / G.ch;
+    G.n_items = ncols * nch;
+    const int64_t grid = std::min<int64_t>(G.n_items, grid_max);
+    k<<<(unsigned)grid, (H + 1) * 32, smem, st>>>(G, rs, ci, q, out, carry, ncarry);
+    return launch_check("sb_bs6_gather_sweep");
+}
+
+}  // namespace
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+int sb_bs6_gather_sweep(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_lo, int32_t c_hi,
+                        const int32_t *row_starts, const int32_t *col_ids, int64_t ng, int64_t nl,
+                        const double *q_local, double *out, const double *carry_in, int64_t n_carry,
+                        sb_stream_t stream) {
+    clear_error();
+    const int64_t g = (int64_t)K * p + 1, n3 = (int64_t)(p + 1) * (p + 1) * (p + 1);
+    if (K < 1 || p < 1 || p > 2 || z0 < 0 || z1 > K || z0 >= z1 || c_lo < 0 || c_hi > g || c_lo >= c_hi) {
+        set_error("sb_bs6_gather_sweep: invalid geometry (K=%d p=%d z=[%d,%d) c=[%d,%d); p must be 1 or 2)", K, p,
+                  z0, z1, c_lo, c_hi);
+        return SB_E_INVALID;
+    }
+    if (ng != (int64_t)(c_hi - c_lo) * g * g || nl != (int64_t)K * K * (z1 - z0) * n3 || nl > INT_MAX ||
+        n_carry < 0 || (n_carry > 0 && !carry_in) || !row_starts || !col_ids || !q_local || !out) {
+        set_error("sb_bs6_gather_sweep: invalid arguments (ng=%lld nl=%lld do not match the geometry)",
+                  (long long)ng, (long long)nl);
+        return SB_E_INVALID;
+    }
+    if (!aligned16(q_local)) {
+        set_error("sb_bs6_gather_sweep: q_local must be 16-byte aligned");
+        return SB_E_INVALID;
+    }
+    if (n_carry > ng) n_carry = ng;
+    SwGeom G{};
+    G.K = K;
+    G.z0 = z0;
+    G.z1 = z1;
+    G.c_lo = c_lo;
+    G.c_hi = c_hi;
+    G.g = (int)g;
+    G.na = (int)((g + kSwW - 1) / kSwW);
+    G.nb = (int)((g + kSwH - 1) / kSwH);
+    G.nl = nl;
+    G.nslot = g_sw_slots > 0 ? g_sw_slots : 4;
+    G.pfd = g_sw_pfd >= 0 ? g_sw_pfd : 4;
+    const bool swz = g_sw_swz >= 0 ? g_sw_swz == 1 : p == 1;
+    const cudaStream_t st = as_stream(stream);
+    return p == 1 ? sweep_launch<1>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, st)
+                  : sweep_launch<2>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, st);
+}
+
+int sb_bs6_sweep_tune(int32_t slots, int32_t l2_prefetch_planes, int32_t waves, int32_t swizzle) {
+    clear_error();
+    if (slots > kSwMaxSlots || (slots > 0 && slots < 3)) {
+        set_error("sb_bs6_sweep_tune: slots must be 3..%d (0: default)", kSwMaxSlots);
+        return SB_E_INVALID;
+    }
+    g_sw_slots = slots;
+    g_sw_pfd = l2_prefetch_planes;
+    g_sw_waves = waves;
+    g_sw_swz = swizzle;
+    return SB_OK;
+}
+
+}  // extern "C"

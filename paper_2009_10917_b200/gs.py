@@ -9,6 +9,8 @@ device GatherOp/ScatterIds or the reference's numpy ones (staged per call).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -21,6 +23,18 @@ def _dev_int(a, name, device):
     return _lib.stage(a, torch.int32, name, device).dev
 
 
+def sweep_geometry(op, q_local):
+    """(K, p, z0, z1, c_lo, c_hi) when the z-sweep kernel (csrc/sb_gs_sweep.cu)
+    takes this gather: a structured device operator of order p <= 2.  Opt-in
+    (SB200_BS6_SWEEP=1) while it measures slower than the super-block kernel
+    (profiles/r02_bs6_sweep.md)."""
+    geo = getattr(op, "geometry", None)
+    if (geo is None or geo[1] > 2 or os.environ.get("SB200_BS6_SWEEP", "0") != "1"
+            or not (op.row_starts.is_cuda and op.col_ids.is_cuda) or q_local.data_ptr() % 16):
+        return None
+    return geo
+
+
 @_lib.device_guard
 def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) -> torch.Tensor:
     """Device-only BS6 writing `out` (length op.ng); optional carry-in partials
@@ -28,6 +42,13 @@ def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) ->
     dev = q_local.device
     L = _lib.lib()
     ncarry = 0 if carry is None else int(carry.shape[0])
+    geo = sweep_geometry(op, q_local)
+    if geo is not None:
+        _lib.check(L.sb_bs6_gather_sweep(*geo, op.row_starts.data_ptr(), op.col_ids.data_ptr(), op.ng,
+                                         int(q_local.shape[0]), q_local.data_ptr(), out.data_ptr(),
+                                         None if carry is None else carry.data_ptr(), ncarry,
+                                         _lib.stream_handle(dev)), "bs6_gather")
+        return out
     st = op.staged() if hasattr(op, "staged") and q_local.data_ptr() % 16 == 0 else None
     if st is not None:
         info, splan = st

@@ -279,3 +279,48 @@ def test_planned_bs6_many_empty_rows_falls_back(sb, oracle):
     out = torch.empty(ng, dtype=torch.float64, device="cuda")
     bs6_gather_into(op, d(q), out)
     assert np.array_equal(h(out), oracle.bs6_gather(rs, ci, q))
+
+
+@pytest.mark.parametrize("carry_rows", [0, 700])
+def test_planned_bs6_abi_oversize_trailer(sb, oracle, carry_rows):
+    """The C-ABI planned gather on an operator with > 512 (empty) rows per
+    super-block: sb_bs6_make_plan flags it in the plan trailer and every
+    kernel variant sums rows from global memory -- bitwise, carry included."""
+    from paper_2009_10917_b200 import _lib
+    ng, nl = 5000, 3000
+    rng = np.random.default_rng(19)
+    l2g = np.sort(rng.choice(ng, nl, replace=False)).astype(np.int32)
+    rs = np.concatenate([[0], np.cumsum(np.bincount(l2g, minlength=ng))]).astype(np.int32)
+    ci = np.argsort(l2g, kind="stable").astype(np.int32)
+    bst = np.append(np.arange(0, ng, 16, dtype=np.int32), ng).astype(np.int32)  # hand-built: 16 rows per block
+    npb = 8
+    L = _lib.lib()
+    size = int(L.sb_bs6_plan_size(bst.shape[0] - 1, npb))
+    plan = torch.full((size,), -7, dtype=torch.int32, device="cuda")
+    rs_d, ci_d, bst_d = (torch.from_numpy(a).cuda() for a in (rs, ci, bst))
+    _lib.check(L.sb_bs6_make_plan(bst_d.data_ptr(), bst.shape[0] - 1, rs_d.data_ptr(), npb, plan.data_ptr(),
+                                  _lib.stream_handle()), "plan")
+    assert int(plan[-2].item()) == 1  # 64 blocks of 16 rows: 1024-row super-blocks
+    q = rng.uniform(-1, 1, nl)
+    carry = rng.uniform(-1, 1, carry_rows) if carry_rows else None
+    want = oracle.bs6_gather(rs, ci, q)
+    for r in range(carry_rows):
+        acc = carry[r]
+        for j in range(rs[r], rs[r + 1]):
+            acc = acc + q[ci[j]]
+        want[r] = acc
+    q_d = d(q)
+    carry_d = None if carry is None else d(carry)
+    for cfg in ("lanes,0,12", "lanes,1,8", "pairs,1,12", "wide,1,6", None):
+        import os
+        if cfg:
+            os.environ["SB200_BS6_CFG"] = cfg
+        try:
+            out = torch.full((ng,), float("nan"), dtype=torch.float64, device="cuda")
+            _lib.check(L.sb_bs6_gather_planned(plan.data_ptr(), bst.shape[0] - 1, npb, rs_d.data_ptr(),
+                                               ci_d.data_ptr(), ng, nl, q_d.data_ptr(), out.data_ptr(),
+                                               None if carry_d is None else carry_d.data_ptr(), carry_rows,
+                                               _lib.stream_handle()), "gather")
+            assert np.array_equal(h(out), want), cfg
+        finally:
+            os.environ.pop("SB200_BS6_CFG", None)
