@@ -169,8 +169,10 @@ int sb_bs6_gather_sweep(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_
 /* Process-wide knobs of sb_bs6_gather_sweep for A/B runs (not thread-safe;
  * 0 / -1 restore the measured defaults): shared-memory ring slots (3..8,
  * default 4), L2 prefetch distance in element planes (-1: 4; 0: off), work
- * items per resident CTA (default 8), value-tile swizzle (-1: for p = 1). */
-int sb_bs6_sweep_tune(int32_t slots, int32_t l2_prefetch_planes, int32_t waves, int32_t swizzle);
+ * items per resident CTA (default 8), value-tile swizzle (-1: for p = 1),
+ * row lines per column = consumer warps per CTA (7, 8 or 16; 0: 8). */
+int sb_bs6_sweep_tune(int32_t slots, int32_t l2_prefetch_planes, int32_t waves, int32_t swizzle,
+                      int32_t row_lines);
 
 /* gs.py:42-61 bs7_scatter(ids, q_global, q_local): q_local[n] =
  * q_global[ids[n]] where ids[n] >= 0 (masked entries untouched).  The caller

@@ -261,6 +261,33 @@ __device__ __forceinline__ bool sw_step(const SwGeom &G, SwState<P, H> &S, SwCur
             dd[1] = s0 + G.rs_d + (cb[1] & 1) - cb[1];
             dd[2] = s2 + (cb[2] & 1) - cb[2];
             dd[3] = s2 + G.rs_d + (cb[3] & 1) - cb[3];
+            bool fast = false;
+            if constexpr (P == 1) {
+                // A structured interior warp-step -- 32 rows of 8 entries each
+                // in the closed-form order (mesh.py:113-134: element (a-1+dx,
+                // b-1+dy, c-1+dz), node (1-dx, 1-dy, 1-dz), entry dz*4+dy*2+dx)
+                // -- is verified against the loaded row starts and columns
+                // (one compare per entry) and then needs no run search: entry
+                // lane + 32 j has run (lane & 7) >> 1 for every j.
+                if (nrows == kSwW && z2 && y2 && I.a0 >= 1 && I.a0 + kSwW <= G.g - 1 && ne == kSwVt) {
+                    const int X = c00 + 7 + 8 * (lane >> 3) + ((lane >> 2) & 1) * (zstride - 4) +
+                                  ((lane >> 1) & 1) * (ystride - 2) + (lane & 1) * 7;
+                    bool ok = lo0 == e0 + 8 * lane;
+#pragma unroll
+                    for (int j = 0; j < E; j++) ok = ok && colA[j] == X + 32 * j;
+                    fast = __all_sync(0xffffffffu, ok);
+                }
+            }
+            if (fast) {
+                const int D = (lane & 4) ? ((lane & 2) ? dd[3] : dd[2]) : ((lane & 2) ? dd[1] : dd[0]);
+#pragma unroll
+                for (int j = 0; j < E; j++) vt[vslot<SWZ>(lane + 32 * j)] = ring[colA[j] + D];
+                __syncwarp();
+#pragma unroll
+                for (int t = 0; t < 8; t++) acc = add(acc, vt[vslot<SWZ>(8 * lane + t)]);
+                st_stream(out + r, acc);
+                __syncwarp();
+            } else {
             // branch-free except for columns outside the runs (a warp vote)
 #pragma unroll
             for (int j = 0; j < E; j++) {
@@ -298,6 +325,7 @@ __device__ __forceinline__ bool sw_step(const SwGeom &G, SwState<P, H> &S, SwCur
                 if (lane < nrows) st_stream(out + r, acc);
             }
             __syncwarp();
+            }
         } else if (lane < nrows) {  // long rows: straight from global memory
 #pragma unroll 1
             for (int t = lo0; t < nxt; t++) acc = add(acc, __ldg(q + __ldg(ci + t)));
@@ -325,8 +353,8 @@ __device__ __forceinline__ bool sw_step(const SwGeom &G, SwState<P, H> &S, SwCur
     return true;
 }
 
-template <int P, int H, bool SWZ>
-__global__ void __launch_bounds__((H + 1) * 32, 2)
+template <int P, int H, bool SWZ, int MB>
+__global__ void __launch_bounds__((H + 1) * 32, MB)
     k_bs6_sweep(SwGeom G, const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
                 const double *__restrict__ q, double *__restrict__ out, const double *__restrict__ carry,
                 int64_t ncarry) {
@@ -439,16 +467,14 @@ __global__ void __launch_bounds__((H + 1) * 32, 2)
     }
 }
 
-constexpr int kSwH = 8;
-
 // tuning knobs (sb_bs6_sweep_tune; A/B runs and tests): <= 0 / < 0 = default
-int g_sw_slots = 0, g_sw_pfd = -1, g_sw_waves = 0, g_sw_swz = -1;
+int g_sw_slots = 0, g_sw_pfd = -1, g_sw_waves = 0, g_sw_swz = -1, g_sw_h = 0;
 
-template <int P>
+template <int P, int H, int MB>
 int sweep_launch(const SwGeom &G0, const int32_t *rs, const int32_t *ci, const double *q, double *out,
                  const double *carry, int64_t ncarry, bool swz, cudaStream_t st) {
-    constexpr int H = kSwH;
     SwGeom G = G0;
+    G.nb = (G.g + H - 1) / H;
     constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
     const int nx_max = (kSwW - 1) / P + 2, ny_max = (H - 1) / P + 2;
     G.rs_d = (nx_max * N3 + 2 + 15) / 16 * 16;  // + the odd-start shift and 16 B rounding
@@ -456,7 +482,7 @@ int sweep_launch(const SwGeom &G0, const int32_t *rs, const int32_t *ci, const d
     const size_t smem = kSwHdr + (size_t)G.nslot * G.plane_d * 8 + (size_t)H * kSwVt * 8;
     using KernT = void (*)(SwGeom, const int32_t *, const int32_t *, const double *, double *, const double *,
                            int64_t);
-    const KernT k = swz ? k_bs6_sweep<P, H, true> : k_bs6_sweep<P, H, false>;
+    const KernT k = swz ? k_bs6_sweep<P, H, true, MB> : k_bs6_sweep<P, H, false, MB>;
     int rc = cuda_check(cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                         "sb_bs6_gather_sweep: shared memory");
     if (rc) return rc;
@@ -514,17 +540,24 @@ int sb_bs6_gather_sweep(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_
     G.c_hi = c_hi;
     G.g = (int)g;
     G.na = (int)((g + kSwW - 1) / kSwW);
-    G.nb = (int)((g + kSwH - 1) / kSwH);
     G.nl = nl;
     G.nslot = g_sw_slots > 0 ? g_sw_slots : 4;
     G.pfd = g_sw_pfd >= 0 ? g_sw_pfd : 4;
     const bool swz = g_sw_swz >= 0 ? g_sw_swz == 1 : p == 1;
     const cudaStream_t st = as_stream(stream);
-    return p == 1 ? sweep_launch<1>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, st)
-                  : sweep_launch<2>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, st);
+    // row lines per column (one consumer warp each) and CTAs per SM: 8 / 2 by
+    // default; 7 / 3 and 16 / 1 for A/B runs
+    const int h = g_sw_h > 0 ? g_sw_h : 8;
+#define SB_SW(P_) (h == 7 ? sweep_launch<P_, 7, 3>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, st) \
+                  : h == 16 ? sweep_launch<P_, 16, 1>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, st) \
+                            : sweep_launch<P_, 8, 2>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, st))
+    const int rc = p == 1 ? SB_SW(1) : SB_SW(2);
+#undef SB_SW
+    return rc;
 }
 
-int sb_bs6_sweep_tune(int32_t slots, int32_t l2_prefetch_planes, int32_t waves, int32_t swizzle) {
+int sb_bs6_sweep_tune(int32_t slots, int32_t l2_prefetch_planes, int32_t waves, int32_t swizzle,
+                      int32_t row_lines) {
     clear_error();
     if (slots > kSwMaxSlots || (slots > 0 && slots < 3)) {
         set_error("sb_bs6_sweep_tune: slots must be 3..%d (0: default)", kSwMaxSlots);
@@ -534,6 +567,7 @@ int sb_bs6_sweep_tune(int32_t slots, int32_t l2_prefetch_planes, int32_t waves, 
     g_sw_pfd = l2_prefetch_planes;
     g_sw_waves = waves;
     g_sw_swz = swizzle;
+    g_sw_h = (row_lines == 7 || row_lines == 8 || row_lines == 16) ? row_lines : 0;
     return SB_OK;
 }
 

@@ -54,8 +54,8 @@ def main():
         ms = timed(planned)
         print(f"N={p:2d} K={K} planned                 {ms:.3f} ms {nb / ms / 1e6:7.0f} GB/s", flush=True)
         for cfg in (cfgs.split(";") if p <= 2 else []):
-            slots, pfd, waves, swz = (int(v) for v in cfg.split(","))
-            _lib.check(L.sb_bs6_sweep_tune(slots, pfd, waves, swz), "tune")
+            slots, pfd, waves, swz, h = (int(v) for v in (cfg + ",0").split(",")[:5])
+            _lib.check(L.sb_bs6_sweep_tune(slots, pfd, waves, swz, h), "tune")
 
             def sweep():
                 rc = L.sb_bs6_gather_sweep(*op.geometry, op.row_starts.data_ptr(), op.col_ids.data_ptr(), op.ng,
@@ -69,7 +69,7 @@ def main():
             ms = timed(sweep)
             print(f"N={p:2d} K={K} sweep {cfg:>16s}  {ms:.3f} ms {nb / ms / 1e6:7.0f} GB/s  bitwise={ok}",
                   flush=True)
-        _lib.check(L.sb_bs6_sweep_tune(0, -1, 0, -1), "tune")
+        _lib.check(L.sb_bs6_sweep_tune(0, -1, 0, -1, 0), "tune")
 
 
 if __name__ == "__main__":

@@ -29,8 +29,8 @@ def tune(sb):
     from paper_2009_10917_b200 import _lib
     L = _lib.lib()
 
-    def set_(slots=0, pfd=-1, waves=0, swz=-1):
-        _lib.check(L.sb_bs6_sweep_tune(slots, pfd, waves, swz), "tune")
+    def set_(slots=0, pfd=-1, waves=0, swz=-1, h=0):
+        _lib.check(L.sb_bs6_sweep_tune(slots, pfd, waves, swz, h), "tune")
     yield set_
     set_()
 
@@ -79,11 +79,11 @@ def test_sweep_whole_mesh_bitwise(sb, oracle, K, p):
     assert np.array_equal(h(out), expect(oracle, op.row_starts, op.col_ids, q))
 
 
-@pytest.mark.parametrize("slots,pfd,waves,swz", [(3, 0, 1, -1), (3, 4, 64, 0), (5, 1, 2, 1), (8, 16, 8, -1),
-                                                 (4, 0, 1000, 1)])
-@pytest.mark.parametrize("K,p", [(13, 1), (11, 2)])
-def test_sweep_ring_and_prefetch_settings(sb, oracle, tune, K, p, slots, pfd, waves, swz):
-    tune(slots, pfd, waves, swz)
+@pytest.mark.parametrize("slots,pfd,waves,swz,h", [(3, 0, 1, -1, 0), (3, 4, 64, 0, 7), (5, 1, 2, 1, 16),
+                                                   (8, 16, 8, -1, 8), (4, 0, 1000, 1, 7), (3, 2, 3, -1, 16)])
+@pytest.mark.parametrize("K,p", [(13, 1), (11, 2), (34, 1)])
+def test_sweep_ring_and_prefetch_settings(sb, oracle, tune, K, p, slots, pfd, waves, swz, h):
+    tune(slots, pfd, waves, swz, h)
     mesh = sb.build_mesh(K, p)
     op = sb.build_gather(mesh)
     q = d(np.random.default_rng([K, p, 72]).uniform(-1, 1, mesh.nl))
@@ -184,7 +184,7 @@ def test_sweep_rejects_bad_geometry(sb):
         with pytest.raises(ValueError):
             sweep(geo, op.row_starts, op.col_ids, ng, nl, q)
     with pytest.raises(ValueError):
-        _lib.check(_lib.lib().sb_bs6_sweep_tune(2, -1, 0, -1), "tune")
+        _lib.check(_lib.lib().sb_bs6_sweep_tune(2, -1, 0, -1, 0), "tune")
 
 
 @pytest.mark.slow
