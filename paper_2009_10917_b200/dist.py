@@ -253,8 +253,8 @@ def gather_raw(op, q: torch.Tensor, out_ptr: int, carry_ptr: int | None, ncarry:
     plan = op.plan()
     if plan is None:
         raise ValueError("the NVLink carry path needs a planned gather operator")
-    _lib.check(L.sb_bs6_gather_planned(plan.data_ptr(), op.n_blocks, op.nodes_per_block, op.row_starts.data_ptr(),
-                                       op.col_ids.data_ptr(), op.ng, op.nl, q.data_ptr(), out_ptr, carry_ptr,
+    _lib.check(L.sb_bs6_gather_planned(plan.data_ptr(), op.n_blocks, op.nodes_per_block, op.row_starts_dev.data_ptr(),
+                                       op.col_ids_dev.data_ptr(), op.ng, op.nl, q.data_ptr(), out_ptr, carry_ptr,
                                        ncarry, _lib.stream_handle(q.device)), "bs6_gather (NVLink carry)")
 
 

@@ -23,6 +23,14 @@ def _dev_int(a, name, device):
     return _lib.stage(a, torch.int32, name, device).dev
 
 
+def _op_dev(op, name, device):
+    """Index array `name` of an operator on the device: this package's
+    operators keep it there (`<name>_dev`); the reference's numpy ones are
+    staged per call."""
+    d = getattr(op, name + "_dev", None)
+    return d if d is not None else _dev_int(getattr(op, name), name, device)
+
+
 def sweep_geometry(op, q_local):
     """(K, p, z0, z1, c_lo, c_hi) when the z-sweep kernel (csrc/sb_gs_sweep.cu)
     takes this gather: a structured device operator of order p <= 2.  Opt-in
@@ -30,7 +38,7 @@ def sweep_geometry(op, q_local):
     (profiles/r02_bs6_sweep.md)."""
     geo = getattr(op, "geometry", None)
     if (geo is None or geo[1] > 2 or os.environ.get("SB200_BS6_SWEEP", "0") != "1"
-            or not (op.row_starts.is_cuda and op.col_ids.is_cuda) or q_local.data_ptr() % 16):
+            or q_local.data_ptr() % 16):
         return None
     return geo
 
@@ -44,7 +52,7 @@ def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) ->
     ncarry = 0 if carry is None else int(carry.shape[0])
     geo = sweep_geometry(op, q_local)
     if geo is not None:
-        _lib.check(L.sb_bs6_gather_sweep(*geo, op.row_starts.data_ptr(), op.col_ids.data_ptr(), op.ng,
+        _lib.check(L.sb_bs6_gather_sweep(*geo, op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(), op.ng,
                                          int(q_local.shape[0]), q_local.data_ptr(), out.data_ptr(),
                                          None if carry is None else carry.data_ptr(), ncarry,
                                          _lib.stream_handle(dev)), "bs6_gather")
@@ -52,22 +60,22 @@ def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) ->
     st = op.staged() if hasattr(op, "staged") and q_local.data_ptr() % 16 == 0 else None
     if st is not None:
         info, splan = st
-        _lib.check(L.sb_bs6_gather_staged(info, splan.data_ptr(), op.row_starts.data_ptr(),
-                                          op.col_ids.data_ptr(), op.ng, op.nl, q_local.data_ptr(),
+        _lib.check(L.sb_bs6_gather_staged(info, splan.data_ptr(), op.row_starts_dev.data_ptr(),
+                                          op.col_ids_dev.data_ptr(), op.ng, op.nl, q_local.data_ptr(),
                                           out.data_ptr(), None if carry is None else carry.data_ptr(),
                                           ncarry, _lib.stream_handle(dev)), "bs6_gather")
         return out
     plan = op.plan() if hasattr(op, "plan") else None
     if plan is not None:
         _lib.check(L.sb_bs6_gather_planned(plan.data_ptr(), op.n_blocks, op.nodes_per_block,
-                                           op.row_starts.data_ptr(), op.col_ids.data_ptr(), op.ng,
+                                           op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(), op.ng,
                                            op.nl, q_local.data_ptr(), out.data_ptr(),
                                            None if carry is None else carry.data_ptr(), ncarry,
                                            _lib.stream_handle(dev)), "bs6_gather")
         return out
-    bst = _dev_int(op.block_starts, "block_starts", dev)
-    rs = _dev_int(op.row_starts, "row_starts", dev)
-    ci = _dev_int(op.col_ids, "col_ids", dev)
+    bst = _op_dev(op, "block_starts", dev)
+    rs = _op_dev(op, "row_starts", dev)
+    ci = _op_dev(op, "col_ids", dev)
     _lib.check(L.sb_bs6_gather(bst.data_ptr(), int(bst.shape[0]) - 1, rs.data_ptr(), ci.data_ptr(),
                                op.ng, int(ci.shape[0]), op.nodes_per_block, q_local.data_ptr(),
                                out.data_ptr(), None if carry is None else carry.data_ptr(), ncarry,
@@ -86,14 +94,15 @@ def _bs6_host_jobs(op):
     """Row chunks of ~CHUNK rows on block boundaries + the q prefix each needs (cached)."""
     jobs = op.__dict__.get("_host_jobs")
     if jobs is None:
-        bst = op.block_starts.cpu().numpy()
+        bst = op.block_starts  # (numpy host view)
         cuts = [0]
         for b in range(1, bst.shape[0]):
             if bst[b] - bst[cuts[-1]] >= hoststream.CHUNK or b == bst.shape[0] - 1:
                 cuts.append(b)
         rows = [int(bst[c]) for c in cuts]
-        ends = op.row_starts[torch.as_tensor(rows[1:], device=op.row_starts.device)].tolist()
-        need = _prefix_need(op.col_ids, ends)
+        rs = op.row_starts_dev
+        ends = rs[torch.as_tensor(rows[1:], device=rs.device)].tolist()
+        need = _prefix_need(op.col_ids_dev, ends)
         jobs = [(rows[i], rows[i + 1], need[i], cuts[i], cuts[i + 1]) for i in range(len(cuts) - 1)]
         object.__setattr__(op, "_host_jobs", jobs)
     return jobs
@@ -102,7 +111,7 @@ def _bs6_host_jobs(op):
 def _bs6_host(op, q_local):
     """Host q_local -> host result, upload / row-chunk gathers / download overlapped."""
     hq = hoststream.as_host_tensor(q_local, "q_local")
-    dev = op.row_starts.device
+    dev = op.row_starts_dev.device
     L = _lib.lib()
     qd = torch.empty(op.nl, dtype=torch.float64, device=dev)
     outd = torch.empty(op.ng, dtype=torch.float64, device=dev)
@@ -114,8 +123,8 @@ def _bs6_host(op, q_local):
 
     def launch(r_lo, r_hi):
         b_lo, b_hi = blocks[r_lo]
-        _lib.check(L.sb_bs6_gather(op.block_starts.data_ptr() + 4 * b_lo, b_hi - b_lo,
-                                   op.row_starts.data_ptr(), op.col_ids.data_ptr(), op.ng, op.nl,
+        _lib.check(L.sb_bs6_gather(op.block_starts_dev.data_ptr() + 4 * b_lo, b_hi - b_lo,
+                                   op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(), op.ng, op.nl,
                                    op.nodes_per_block, qd.data_ptr(), outd.data_ptr(), None, 0,
                                    _lib.stream_handle(dev)), "bs6_gather")
 
@@ -129,7 +138,7 @@ def bs6_gather(op, q_local, out=None):
     if q_local.shape[0] != op.nl:
         raise ValueError(f"local vector length {q_local.shape[0]} != operator NL {op.nl}")
     host = not (isinstance(q_local, torch.Tensor) and q_local.is_cuda)
-    if host and out is None and isinstance(op.row_starts, torch.Tensor) and op.row_starts.is_cuda:
+    if host and out is None and hasattr(op, "row_starts_dev"):
         return _bs6_host(op, q_local)
     q = _lib.stage(q_local, torch.float64, "q_local").dev
     if out is None:
@@ -150,12 +159,12 @@ def _bs7_host(ids, q_global, q_local) -> None:
     and q_local download overlapped (q_local is write-only, never uploaded)."""
     hg = hoststream.as_host_tensor(q_global, "q_global")
     hl = hoststream.as_host_tensor(q_local, "q_local")
-    dev = ids.ids.device
+    dev = ids.ids_dev.device
     nl, ng = ids.nl, int(hg.shape[0])
     jobs = ids.__dict__.get("_host_jobs")
     if jobs is None:
         cuts = list(range(0, nl, hoststream.CHUNK)) + [nl]
-        need = _prefix_need(ids.ids, cuts[1:])
+        need = _prefix_need(ids.ids_dev, cuts[1:])
         jobs = [(cuts[i], cuts[i + 1], need[i]) for i in range(len(cuts) - 1)]
         ids.__dict__["_host_jobs"] = jobs
     L = _lib.lib()
@@ -163,7 +172,7 @@ def _bs7_host(ids, q_global, q_local) -> None:
     ld = torch.empty(nl, dtype=torch.float64, device=dev)
 
     def launch(lo, hi):
-        _lib.check(L.sb_bs7_scatter(ids.ids.data_ptr() + 4 * lo, hi - lo, gd.data_ptr(), ng,
+        _lib.check(L.sb_bs7_scatter(ids.ids_dev.data_ptr() + 4 * lo, hi - lo, gd.data_ptr(), ng,
                                     ld.data_ptr() + 8 * lo, 0, _lib.stream_handle(dev)), "bs7_scatter")
 
     hoststream.run_prefix(hg, gd, ld, hl, jobs, launch, dev)
@@ -181,7 +190,7 @@ def bs7_scatter(ids, q_global, q_local) -> None:
     if ids.nl and max_id >= ng:
         raise ValueError(f"scatter id {max_id} out of range [0, {ng})")
     if (hoststream.all_host(q_global, q_local) and not ids.has_mask
-            and isinstance(ids.ids, torch.Tensor) and ids.ids.is_cuda and ids.ids.data_ptr() % 16 == 0):
+            and hasattr(ids, "ids_dev") and ids.ids_dev.data_ptr() % 16 == 0):
         _bs7_host(ids, q_global, q_local)
         return
     sg = _lib.stage(q_global, torch.float64, "q_global")
@@ -195,7 +204,7 @@ def bs7_scatter(ids, q_global, q_local) -> None:
                          "cpu" if isinstance(host, torch.Tensor) else "numpy")
     else:
         sl = _lib.stage(q_local, torch.float64, "q_local", dev)
-    id_t = _dev_int(ids.ids, "ids", dev)
+    id_t = _op_dev(ids, "ids", dev)
     L = _lib.lib()
     _lib.check(L.sb_bs7_scatter(id_t.data_ptr(), int(id_t.shape[0]), sg.dev.data_ptr(), ng,
                                 sl.dev.data_ptr(), int(bool(ids.has_mask)),

@@ -15,7 +15,7 @@ reference's greedy rule in both cases (sb_build_block_starts).
 from __future__ import annotations
 
 import os
-from dataclasses import dataclass, field
+from dataclasses import FrozenInstanceError
 from functools import cached_property
 
 import numpy as np
@@ -33,41 +33,115 @@ def _dev(device=None) -> torch.device:
     return torch.device(device)
 
 
-@dataclass(frozen=True)
-class MeshConnectivity:
+def _l2g_dev(mesh) -> torch.Tensor:
+    """The mesh's local_to_global on the device (this package's mesh, or the
+    reference's numpy one, uploaded)."""
+    d = getattr(mesh, "local_to_global_dev", None)
+    if d is not None:
+        return d
+    return torch.from_numpy(np.ascontiguousarray(mesh.local_to_global, dtype=np.int32)).to(_dev())
+
+
+class _IndexArrays:
+    """Frozen holder of int32 index arrays (the reference's frozen dataclasses,
+    mesh.py:20-70).  The builders here make every array on the device; the
+    reference's attribute names (local_to_global, ids, row_starts, ...) are
+    numpy host views, downloaded once on first access, so reference-style
+    numpy code works unchanged, while the kernels use the `<name>_dev` CUDA
+    tensors and never pay the copy.  Arrays passed in as numpy are uploaded
+    once on first device use instead."""
+
+    _ARRAYS: tuple[str, ...] = ()
+
+    def _init_arrays(self, **arrays) -> None:
+        for name, a in arrays.items():
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                dev, host = a, None
+            else:
+                host = a.numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+                if host.dtype != np.int32:
+                    host = host.astype(np.int32)
+                dev = None
+            object.__setattr__(self, f"_{name}_d", dev)
+            object.__setattr__(self, f"_{name}_h", host)
+
+    def __setattr__(self, name, value):
+        raise FrozenInstanceError(f"cannot assign to field {name!r}")
+
+    def _host(self, name: str) -> np.ndarray:
+        h = self.__dict__[f"_{name}_h"]
+        if h is None:
+            h = self.__dict__[f"_{name}_d"].cpu().numpy()
+            object.__setattr__(self, f"_{name}_h", h)
+        return h
+
+    def _device(self, name: str) -> torch.Tensor:
+        d = self.__dict__[f"_{name}_d"]
+        if d is None:
+            d = torch.from_numpy(np.ascontiguousarray(self.__dict__[f"_{name}_h"])).to(_dev())
+            object.__setattr__(self, f"_{name}_d", d)
+        return d
+
+    def _length(self, name: str) -> int:
+        d = self.__dict__[f"_{name}_d"]
+        return int(d.shape[0]) if d is not None else int(self.__dict__[f"_{name}_h"].shape[0])
+
+
+def _host_view(name: str, doc: str) -> property:
+    return property(lambda self: self._host(name), doc=f"{doc} (numpy int32 host view)")
+
+
+def _device_view(name: str, doc: str) -> property:
+    return property(lambda self: self._device(name), doc=f"{doc} (int32 CUDA tensor)")
+
+
+class MeshConnectivity(_IndexArrays):
     """mesh.py:20-36: element-local to global node numbering for a K^3 mesh of order p."""
 
-    K: int
-    p: int
-    local_to_global: torch.Tensor = field(repr=False)
-    # True when local_to_global is the build_mesh numbering (enables the
-    # closed-form operator builder); user-supplied maps use the general path.
-    structured: bool = field(default=False, repr=False, compare=False)
+    def __init__(self, K: int, p: int, local_to_global, structured: bool = False):
+        object.__setattr__(self, "K", K)
+        object.__setattr__(self, "p", p)
+        # True when local_to_global is the build_mesh numbering (enables the
+        # closed-form operator builder); user-supplied maps use the general path
+        object.__setattr__(self, "structured", structured)
+        self._init_arrays(local_to_global=local_to_global)
+
+    local_to_global = _host_view("local_to_global", "mesh.py:20-36 local-to-global map")
+    local_to_global_dev = _device_view("local_to_global", "local-to-global map")
+
+    def __repr__(self) -> str:
+        return f"MeshConnectivity(K={self.K}, p={self.p})"
 
     @property
     def nl(self) -> int:
-        return int(self.local_to_global.shape[0])
+        return self._length("local_to_global")
 
     @property
     def ng(self) -> int:
         return (self.K * self.p + 1) ** 3
 
 
-@dataclass(frozen=True)
-class ScatterIds:
+class ScatterIds(_IndexArrays):
     """mesh.py:39-51: local-to-global id map; masked entries hold -1."""
 
-    ids: torch.Tensor = field(repr=False)
+    def __init__(self, ids):
+        self._init_arrays(ids=ids)
+
+    ids = _host_view("ids", "mesh.py:39-51 scatter ids")
+    ids_dev = _device_view("ids", "scatter ids")
+
+    def __repr__(self) -> str:
+        return f"ScatterIds(nl={self.nl})"
 
     @property
     def nl(self) -> int:
-        return int(self.ids.shape[0])
+        return self._length("ids")
 
     @cached_property
     def _minmax(self) -> tuple[int, int]:
         # one device reduction per operator (the reference re-scans ids on
         # every bs7 call, gs.py:49-50; ids are immutable, so we cache it)
-        ids = self.ids if self.ids.is_cuda else self.ids.cuda()
+        ids = self.ids_dev
         if ids.numel() == 0:
             return (0, -1)
         out = torch.empty(2, dtype=torch.int32, device=ids.device)
@@ -89,26 +163,35 @@ class ScatterIds:
 BS6_PLAN_CAP = 512  # entries (and rows) per super-block, kBs6Cap in csrc/sb_gs_pipe.cu
 
 
-@dataclass(frozen=True)
-class GatherOp:
+class GatherOp(_IndexArrays):
     """mesh.py:54-70: CSR of the gather operator with row blocks of bounded nonzero count."""
 
-    ng: int
-    row_starts: torch.Tensor = field(repr=False)
-    col_ids: torch.Tensor = field(repr=False)
-    block_starts: torch.Tensor = field(repr=False)
-    nodes_per_block: int
-    # (K, p, z0, z1, c_lo, c_hi) when the operator is the closed-form CSR of a
-    # build_mesh numbering (or a slab of it): enables the TMA-staged BS6 plan
-    geometry: tuple | None = field(default=None, repr=False, compare=False)
+    def __init__(self, ng: int, row_starts, col_ids, block_starts, nodes_per_block: int,
+                 geometry: tuple | None = None):
+        object.__setattr__(self, "ng", ng)
+        object.__setattr__(self, "nodes_per_block", nodes_per_block)
+        # (K, p, z0, z1, c_lo, c_hi) when the operator is the closed-form CSR of
+        # a build_mesh numbering (or a slab of it): enables the z-sweep kernel
+        object.__setattr__(self, "geometry", geometry)
+        self._init_arrays(row_starts=row_starts, col_ids=col_ids, block_starts=block_starts)
+
+    row_starts = _host_view("row_starts", "mesh.py:54-70 CSR row starts")
+    col_ids = _host_view("col_ids", "mesh.py:54-70 CSR column ids")
+    block_starts = _host_view("block_starts", "mesh.py:54-70 row-block starts")
+    row_starts_dev = _device_view("row_starts", "CSR row starts")
+    col_ids_dev = _device_view("col_ids", "CSR column ids")
+    block_starts_dev = _device_view("block_starts", "row-block starts")
+
+    def __repr__(self) -> str:
+        return f"GatherOp(ng={self.ng}, nl={self.nl}, nodes_per_block={self.nodes_per_block})"
 
     @property
     def nl(self) -> int:
-        return int(self.col_ids.shape[0])
+        return self._length("col_ids")
 
     @property
     def n_blocks(self) -> int:
-        return int(self.block_starts.shape[0]) - 1
+        return self._length("block_starts") - 1
 
     def _superblock_extent(self) -> tuple[int, int]:
         """(rows, entries) of the largest super-block of the BS6 plan (G =
@@ -116,12 +199,12 @@ class GatherOp:
         build_gather; a hand-built one (empty rows, or blocks not packed to
         nodes_per_block) can exceed them and then takes the unplanned path."""
         g = max(1, BS6_PLAN_CAP // self.nodes_per_block)
-        bst = self.block_starts
+        bst = self.block_starts_dev
         idx = torch.arange(0, self.n_blocks + g, g, device=bst.device).clamp_(max=self.n_blocks)
         rows = bst[idx].long()
         if rows.numel() < 2:
             return 0, 0
-        ents = self.row_starts[rows].long()
+        ents = self.row_starts_dev[rows].long()
         return int((rows[1:] - rows[:-1]).max().item()), int((ents[1:] - ents[:-1]).max().item())
 
     def plan(self) -> torch.Tensor | None:
@@ -131,54 +214,51 @@ class GatherOp:
         if p is not False:
             return p
         p = None
-        if (self.row_starts.is_cuda and self.col_ids.is_cuda and self.block_starts.is_cuda
-                and self.row_starts.data_ptr() % 16 == 0 and self.col_ids.data_ptr() % 16 == 0
+        rs, ci = self.row_starts_dev, self.col_ids_dev
+        if (rs.data_ptr() % 16 == 0 and ci.data_ptr() % 16 == 0
                 and os.environ.get("SB200_NO_PIPE") != "1"):
             L = _lib.lib()
             size = int(L.sb_bs6_plan_size(self.n_blocks, self.nodes_per_block))
             if size > 0 and max(self._superblock_extent()) > BS6_PLAN_CAP:
                 size = 0  # a super-block would exceed the kernel's row / entry capacity
             if size > 0:
-                dev = self.row_starts.device
+                dev = rs.device
                 p = torch.empty(size, dtype=torch.int32, device=dev)
-                _lib.check(L.sb_bs6_make_plan(self.block_starts.data_ptr(), self.n_blocks,
-                                              self.row_starts.data_ptr(), self.nodes_per_block,
+                # (synchronises the stream once: the plan is complete for consumers on any stream)
+                _lib.check(L.sb_bs6_make_plan(self.block_starts_dev.data_ptr(), self.n_blocks,
+                                              rs.data_ptr(), self.nodes_per_block,
                                               p.data_ptr(), _lib.stream_handle(dev)), "bs6 plan")
-                # built once per operator; consumers may run on other streams
-                torch.cuda.current_stream(dev).synchronize()
         object.__setattr__(self, "_plan", p)
         return p
-
 
     def staged(self):
         """(sb_bs6_staged_t, plan) of the TMA-staged BS6 kernel
         (csrc/sb_gs_staged.cu), built once per operator; None unless the
-        operator is a structured one of order p <= 2 on the device.  Opt-in
-        (SB200_BS6_STAGED=1): measured slower than the super-block kernel so
-        far (profiles/r02_bs6_staged.md); SB200_BS6_TILE="ey,ez,w" overrides
+        operator is a structured one of order p <= 2.  Opt-in
+        (SB200_BS6_STAGED=1): measured slower than the super-block kernel
+        (profiles/r02_bs6_staged.md); SB200_BS6_TILE="ey,ez,w" overrides
         the tile shape (A/B runs)."""
         st = self.__dict__.get("_staged", False)
         if st is not False:
             return st
         st = None
         geo = self.geometry
-        if (geo is not None and os.environ.get("SB200_BS6_STAGED", "0") == "1"
-                and self.row_starts.is_cuda and self.col_ids.is_cuda
-                and self.row_starts.data_ptr() % 16 == 0 and self.col_ids.data_ptr() % 16 == 0):
-            tile = [int(v) for v in os.environ.get("SB200_BS6_TILE", "0,0,0").split(",")]
-            L = _lib.lib()
-            info = _lib.Bs6Staged()
-            rc = L.sb_bs6_staged_init(*geo, *tile, info)
-            if rc == _lib.SB_OK:
-                dev = self.row_starts.device
-                plan = torch.empty(max(1, info.n_tiles * info.words_per_tile), dtype=torch.int32,
-                                   device=dev)
-                _lib.check(L.sb_bs6_staged_make_plan(info, self.row_starts.data_ptr(),
-                                                     plan.data_ptr(), _lib.stream_handle(dev)),
-                           "bs6 staged plan")
-                # consumers may run on other streams: the plan is complete once built
-                torch.cuda.current_stream(dev).synchronize()
-                st = (info, plan)
+        if geo is not None and os.environ.get("SB200_BS6_STAGED", "0") == "1":
+            rs, ci = self.row_starts_dev, self.col_ids_dev
+            if rs.data_ptr() % 16 == 0 and ci.data_ptr() % 16 == 0:
+                tile = [int(v) for v in os.environ.get("SB200_BS6_TILE", "0,0,0").split(",")]
+                L = _lib.lib()
+                info = _lib.Bs6Staged()
+                rc = L.sb_bs6_staged_init(*geo, *tile, info)
+                if rc == _lib.SB_OK:
+                    dev = rs.device
+                    plan = torch.empty(max(1, info.n_tiles * info.words_per_tile), dtype=torch.int32,
+                                       device=dev)
+                    _lib.check(L.sb_bs6_staged_make_plan(info, rs.data_ptr(), plan.data_ptr(),
+                                                         _lib.stream_handle(dev)), "bs6 staged plan")
+                    # consumers may run on other streams: the plan is complete once built
+                    torch.cuda.current_stream(dev).synchronize()
+                    st = (info, plan)
         object.__setattr__(self, "_staged", st)
         return st
 
@@ -205,10 +285,8 @@ def build_mesh(K: int, p: int, device=None) -> MeshConnectivity:
 @_lib.device_guard
 def build_scatter_ids(mesh: MeshConnectivity, mask=None) -> ScatterIds:
     """mesh.py:100-110: scatter id map for the mesh; global ids in `mask` become -1."""
-    l2g = mesh.local_to_global
-    dev = l2g.device if l2g.is_cuda else _dev()
-    if not l2g.is_cuda:
-        l2g = l2g.to(dev)
+    l2g = _l2g_dev(mesh)
+    dev = l2g.device
     ids = torch.empty_like(l2g)
     L = _lib.lib()
     st = _lib.stream_handle(dev)
@@ -259,13 +337,14 @@ def build_gather(mesh: MeshConnectivity, nodes_per_block: int = 512) -> GatherOp
     take consecutive rows while their nonzeros stay within nodes_per_block.
     """
     ng, nl = mesh.ng, mesh.nl
-    l2g = mesh.local_to_global
-    dev = l2g.device if l2g.is_cuda else _dev()
+    structured = getattr(mesh, "structured", False)
+    l2g = None if structured else _l2g_dev(mesh)
+    dev = _dev() if l2g is None else l2g.device
     L = _lib.lib()
     st = _lib.stream_handle(dev)
     rs = torch.empty(ng + 1, dtype=INDEX_DTYPE, device=dev)
     ci = torch.empty(nl, dtype=INDEX_DTYPE, device=dev)
-    if mesh.structured:
+    if structured:
         longest = _max_row_len(mesh.K)
         if longest > nodes_per_block:
             raise ValueError(f"nodes_per_block={nodes_per_block} is below the longest row "
@@ -273,8 +352,6 @@ def build_gather(mesh: MeshConnectivity, nodes_per_block: int = 512) -> GatherOp
         _lib.check(L.sb_build_gather_csr(mesh.K, mesh.p, 0, mesh.K, 0, mesh.K * mesh.p + 1,
                                          rs.data_ptr(), ci.data_ptr(), st), "build_gather")
     else:
-        if not l2g.is_cuda:
-            l2g = l2g.to(dev)
         tmp = torch.empty(int(L.sb_build_gather_general_temp_bytes(nl)), dtype=torch.uint8,
                           device=dev)
         stats = torch.empty(2, dtype=torch.int64, device=dev)
@@ -288,7 +365,7 @@ def build_gather(mesh: MeshConnectivity, nodes_per_block: int = 512) -> GatherOp
             raise ValueError(f"nodes_per_block={nodes_per_block} is below the longest row "
                              f"({cmax} nonzeros)")
     bst = _block_starts(rs, ng, nodes_per_block)
-    geo = (mesh.K, mesh.p, 0, mesh.K, 0, mesh.K * mesh.p + 1) if mesh.structured else None
+    geo = (mesh.K, mesh.p, 0, mesh.K, 0, mesh.K * mesh.p + 1) if structured else None
     return GatherOp(ng=ng, row_starts=rs, col_ids=ci, block_starts=bst,
                     nodes_per_block=nodes_per_block, geometry=geo)
 
@@ -335,19 +412,25 @@ def build_slab_l2g(K: int, p: int, z0: int, z1: int, device=None) -> torch.Tenso
 
 
 @_lib.device_guard
-def multiplicity(mesh: MeshConnectivity) -> torch.Tensor:
-    """mesh.py:150-153: per-global-node count of element-local copies (float64, device)."""
-    l2g = mesh.local_to_global
-    dev = l2g.device if l2g.is_cuda else _dev()
+def multiplicity_dev(mesh: MeshConnectivity) -> torch.Tensor:
+    """mesh.py:150-153 on the device: per-global-node count of element-local
+    copies (float64 CUDA tensor)."""
+    dev = _dev() if getattr(mesh, "structured", False) else _l2g_dev(mesh).device
     out = torch.empty(mesh.ng, dtype=torch.float64, device=dev)
     L = _lib.lib()
     st = _lib.stream_handle(dev)
-    if mesh.structured:
+    if getattr(mesh, "structured", False):
         _lib.check(L.sb_multiplicity(mesh.K, mesh.p, 0, mesh.K, 0, mesh.K * mesh.p + 1,
                                      out.data_ptr(), st), "multiplicity")
     else:
-        if not l2g.is_cuda:
-            l2g = l2g.to(dev)
+        l2g = _l2g_dev(mesh)
         _lib.check(L.sb_histogram(l2g.data_ptr(), l2g.shape[0], mesh.ng, out.data_ptr(), st),
                    "multiplicity")
     return out
+
+
+def multiplicity(mesh: MeshConnectivity) -> np.ndarray:
+    """mesh.py:150-153: per-global-node count of element-local copies, float64
+    numpy like the reference (computed on the device; multiplicity_dev keeps
+    it there)."""
+    return multiplicity_dev(mesh).cpu().numpy()

@@ -24,8 +24,8 @@ def plan_for(op, G):
     nb = op.n_blocks
     nsb = (nb + G - 1) // G
     idx = torch.clamp(torch.arange(nsb + 1, device="cuda") * G, max=nb)
-    r = op.block_starts[idx].long()
-    e = op.row_starts[r]
+    r = op.block_starts_dev[idx].long()
+    e = op.row_starts_dev[r]
     plan = torch.stack([r.int(), e.int()], 1).reshape(-1).contiguous()
     return plan, nsb
 
@@ -40,14 +40,14 @@ for K, p in [(66, 7), (463, 1), (31, 15)]:
     st = torch.cuda.current_stream()
     for variant, cap, cps in [(7, 512, 0), (12, 512, 0), (13, 512, 0), (14, 1024, 0), (11, 512, 0)]:
         plan, nsb = plan_for(op, max(1, cap // 512))
-        per_sm = L.expt_bs6(variant, plan.data_ptr(), nsb, op.row_starts.data_ptr(), op.col_ids.data_ptr(),
+        per_sm = L.expt_bs6(variant, plan.data_ptr(), nsb, op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(),
                             q.data_ptr(), out.data_ptr(), cps, st.cuda_stream)
         torch.cuda.synchronize()
         ok = torch.equal(out, ref) if variant not in (1, 11) else None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(10):
-            L.expt_bs6(variant, plan.data_ptr(), nsb, op.row_starts.data_ptr(), op.col_ids.data_ptr(),
+            L.expt_bs6(variant, plan.data_ptr(), nsb, op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(),
                        q.data_ptr(), out.data_ptr(), cps, st.cuda_stream)
         e1.record()
         e1.synchronize()

@@ -31,7 +31,7 @@ for K, p in [(66, 7), (463, 1), (31, 15)]:
     out = torch.empty(mesh.ng + 2, dtype=torch.float64, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
     for v in range(5):
-        args = (v, plan.data_ptr(), nsb, op.row_starts.data_ptr(), op.col_ids.data_ptr(), q.data_ptr(),
+        args = (v, plan.data_ptr(), nsb, op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(), q.data_ptr(),
                 out.data_ptr(), mesh.nl, mesh.ng, st)
         assert L.diag_bs6(*args) == 0
         torch.cuda.synchronize()

@@ -23,7 +23,7 @@ for K, p in [(66, 7), (463, 1), (31, 15), (132, 3)]:
     mesh = sb.build_mesh(K, p)
     ids = sb.build_scatter_ids(mesh)
     qg = torch.empty(mesh.ng, dtype=torch.float64, device="cuda").uniform_(-1, 1)
-    ref = qg[mesh.local_to_global.long()]
+    ref = qg[mesh.local_to_global_dev.long()]
     nbytes = bytes_moved("bs7", nl=mesh.nl, ng=mesh.ng)
     ql = torch.empty(mesh.nl, dtype=torch.float64, device="cuda")
     st = torch.cuda.current_stream().cuda_stream

@@ -20,7 +20,7 @@ L.probe.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void
 for K, p in [(463, 1), (232, 2), (66, 7)]:
     mesh = sb.build_mesh(K, p)
     op = sb.build_gather(mesh)
-    ci = op.col_ids
+    ci = op.col_ids_dev
     n = ci.shape[0]
     q = torch.empty(n + 2, dtype=torch.float64, device="cuda").uniform_(-1, 1)
     sink = torch.zeros(1, dtype=torch.float64, device="cuda")

@@ -17,7 +17,7 @@ for p in orders:
     op = sb.build_gather(mesh)
     q = torch.empty(mesh.nl, dtype=torch.float64, device="cuda").uniform_(-1, 1)
     out = sb.bs6_gather(op, q)
-    ref = torch.zeros_like(out).index_add_(0, mesh.local_to_global.long(), q)  # order differs: check closeness
+    ref = torch.zeros_like(out).index_add_(0, mesh.local_to_global_dev.long(), q)  # order differs: check closeness
     err = ((out - ref).abs().max() / ref.abs().max()).item()
     nbytes = bytes_moved("bs6", nl=mesh.nl, ng=mesh.ng)
     for _ in range(3):

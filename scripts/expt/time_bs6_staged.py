@@ -50,8 +50,8 @@ def main():
         st = _lib.stream_handle()
 
         def planned():
-            L.sb_bs6_gather_planned(plan.data_ptr(), op.n_blocks, op.nodes_per_block, op.row_starts.data_ptr(),
-                                    op.col_ids.data_ptr(), op.ng, op.nl, q.data_ptr(), ref.data_ptr(), None, 0, st)
+            L.sb_bs6_gather_planned(plan.data_ptr(), op.n_blocks, op.nodes_per_block, op.row_starts_dev.data_ptr(),
+                                    op.col_ids_dev.data_ptr(), op.ng, op.nl, q.data_ptr(), ref.data_ptr(), None, 0, st)
         ms = timed(planned)
         print(f"N={p:2d} K={K} planned        {ms:.3f} ms {nb / ms / 1e6:7.0f} GB/s", flush=True)
         tiles = [tuple(int(v) for v in t.split(",")) for t in tiles_env.split(";")] if tiles_env else \
@@ -63,13 +63,13 @@ def main():
                 print("  init failed", tile, _lib.last_error())
                 continue
             splan = torch.empty(info.n_tiles * info.words_per_tile, dtype=torch.int32, device="cuda")
-            _lib.check(L.sb_bs6_staged_make_plan(info, op.row_starts.data_ptr(), splan.data_ptr(), st), "plan")
+            _lib.check(L.sb_bs6_staged_make_plan(info, op.row_starts_dev.data_ptr(), splan.data_ptr(), st), "plan")
             out = torch.empty_like(ref)
 
             def staged():
-                L.sb_bs6_gather_staged(info, splan.data_ptr(), op.row_starts.data_ptr(), op.col_ids.data_ptr(),
+                L.sb_bs6_gather_staged(info, splan.data_ptr(), op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(),
                                        op.ng, op.nl, q.data_ptr(), out.data_ptr(), None, 0, st)
-            rc = L.sb_bs6_gather_staged(info, splan.data_ptr(), op.row_starts.data_ptr(), op.col_ids.data_ptr(),
+            rc = L.sb_bs6_gather_staged(info, splan.data_ptr(), op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(),
                                         op.ng, op.nl, q.data_ptr(), out.data_ptr(), None, 0, st)
             if rc != 0:
                 print("  gather failed", tile, _lib.last_error())

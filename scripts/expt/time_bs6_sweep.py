@@ -49,8 +49,8 @@ def main():
         st = _lib.stream_handle()
 
         def planned():
-            L.sb_bs6_gather_planned(plan.data_ptr(), op.n_blocks, op.nodes_per_block, op.row_starts.data_ptr(),
-                                    op.col_ids.data_ptr(), op.ng, op.nl, q.data_ptr(), ref.data_ptr(), None, 0, st)
+            L.sb_bs6_gather_planned(plan.data_ptr(), op.n_blocks, op.nodes_per_block, op.row_starts_dev.data_ptr(),
+                                    op.col_ids_dev.data_ptr(), op.ng, op.nl, q.data_ptr(), ref.data_ptr(), None, 0, st)
         ms = timed(planned)
         print(f"N={p:2d} K={K} planned                 {ms:.3f} ms {nb / ms / 1e6:7.0f} GB/s", flush=True)
         for cfg in (cfgs.split(";") if p <= 2 else []):
@@ -58,7 +58,7 @@ def main():
             _lib.check(L.sb_bs6_sweep_tune(slots, pfd, waves, swz, h), "tune")
 
             def sweep():
-                rc = L.sb_bs6_gather_sweep(*op.geometry, op.row_starts.data_ptr(), op.col_ids.data_ptr(), op.ng,
+                rc = L.sb_bs6_gather_sweep(*op.geometry, op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(), op.ng,
                                            op.nl, q.data_ptr(), out.data_ptr(), None, 0, st)
                 if rc:
                     raise RuntimeError(_lib.last_error())

@@ -18,7 +18,7 @@ for p in orders:
     qg = torch.empty(mesh.ng, dtype=torch.float64, device="cuda").uniform_(-1, 1)
     ql = torch.empty(mesh.nl, dtype=torch.float64, device="cuda")
     sb.bs7_scatter(ids, qg, ql)
-    ok = torch.equal(ql, qg[mesh.local_to_global.long()])
+    ok = torch.equal(ql, qg[mesh.local_to_global_dev.long()])
     nbytes = bytes_moved("bs7", nl=mesh.nl, ng=mesh.ng)
     for _ in range(3):
         sb.bs7_scatter(ids, qg, ql)

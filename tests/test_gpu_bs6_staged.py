@@ -40,13 +40,13 @@ def staged_run(op, q, geo, tile=(0, 0, 0), carry=None, edit_info=None, edit_plan
     if edit_info is not None:
         edit_info(info)
     plan = torch.empty(max(1, info.n_tiles * info.words_per_tile), dtype=torch.int32, device="cuda")
-    _lib.check(L.sb_bs6_staged_make_plan(info, op.row_starts.data_ptr(), plan.data_ptr(),
+    _lib.check(L.sb_bs6_staged_make_plan(info, op.row_starts_dev.data_ptr(), plan.data_ptr(),
                                          _lib.stream_handle()), "plan")
     if edit_plan is not None:
         edit_plan(plan.view(-1, info.words_per_tile), info)
     out = torch.full((op.ng,), float("nan"), dtype=torch.float64, device="cuda")
     nc = 0 if carry is None else int(carry.shape[0])
-    _lib.check(L.sb_bs6_gather_staged(info, plan.data_ptr(), op.row_starts.data_ptr(), op.col_ids.data_ptr(),
+    _lib.check(L.sb_bs6_gather_staged(info, plan.data_ptr(), op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(),
                                       op.ng, op.nl, q.data_ptr(), out.data_ptr(),
                                       None if carry is None else carry.data_ptr(), nc, _lib.stream_handle()),
                "gather")
@@ -54,9 +54,9 @@ def staged_run(op, q, geo, tile=(0, 0, 0), carry=None, edit_info=None, edit_plan
 
 
 def expect(oracle, op, q, carry=None):
-    want = oracle.bs6_gather(h(op.row_starts), h(op.col_ids), h(q))
+    want = oracle.bs6_gather(h(op.row_starts_dev), h(op.col_ids_dev), h(q))
     if carry is not None:  # rows < len(carry) start from the carry instead of +0.0
-        rs, ci, qq, c = h(op.row_starts), h(op.col_ids), h(q), h(carry)
+        rs, ci, qq, c = h(op.row_starts_dev), h(op.col_ids_dev), h(q), h(carry)
         for r in range(c.shape[0]):
             acc = c[r]
             for j in range(rs[r], rs[r + 1]):
@@ -155,10 +155,10 @@ def test_staged_other_csr_same_rows(sb, oracle):
     mesh = sb.build_mesh(K, p)
     op = sb.build_gather(mesh)
     rng = np.random.default_rng(65)
-    ci = h(op.col_ids)
+    ci = h(op.col_ids_dev)
     perm = rng.permutation(ci.shape[0]).astype(np.int32)
     from paper_2009_10917_b200 import mesh as M
-    op2 = M.GatherOp(ng=op.ng, row_starts=op.row_starts, col_ids=d(perm[ci]), block_starts=op.block_starts,
+    op2 = M.GatherOp(ng=op.ng, row_starts=op.row_starts_dev, col_ids=d(perm[ci]), block_starts=op.block_starts_dev,
                      nodes_per_block=op.nodes_per_block, geometry=op.geometry)
     q = d(rng.uniform(-1, 1, mesh.nl))
     out = sb.bs6_gather(op2, q)
@@ -192,7 +192,7 @@ def test_staged_c3_full_size(sb, oracle, p):
         gen.manual_seed(463 + p)
         q = torch.empty(op.nl, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
         out = h(sb.bs6_gather(op, q))
-        want = oracle.bs6_gather(h(op.row_starts), h(op.col_ids), h(q))
+        want = oracle.bs6_gather(h(op.row_starts_dev), h(op.col_ids_dev), h(q))
         assert np.array_equal(out, want)
     finally:
         oracle.set_threads(1)

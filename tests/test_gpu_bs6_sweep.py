@@ -76,19 +76,19 @@ def test_sweep_whole_mesh_bitwise(sb, oracle, K, p):
     q = d(np.random.default_rng([K, p, 71]).uniform(-1, 1, mesh.nl))
     assert sweep_geometry(op, q) == (K, p, 0, K, 0, K * p + 1)  # the public call takes the sweep
     out = sb.bs6_gather(op, q)
-    assert np.array_equal(h(out), expect(oracle, op.row_starts, op.col_ids, q))
+    assert np.array_equal(h(out), expect(oracle, op.row_starts_dev, op.col_ids_dev, q))
 
 
-@pytest.mark.parametrize("slots,pfd,waves,swz,h", [(3, 0, 1, -1, 0), (3, 4, 64, 0, 7), (5, 1, 2, 1, 16),
+@pytest.mark.parametrize("slots,pfd,waves,swz,rows", [(3, 0, 1, -1, 0), (3, 4, 64, 0, 7), (5, 1, 2, 1, 16),
                                                    (8, 16, 8, -1, 8), (4, 0, 1000, 1, 7), (3, 2, 3, -1, 16)])
 @pytest.mark.parametrize("K,p", [(13, 1), (11, 2), (34, 1)])
-def test_sweep_ring_and_prefetch_settings(sb, oracle, tune, K, p, slots, pfd, waves, swz, h):
-    tune(slots, pfd, waves, swz, h)
+def test_sweep_ring_and_prefetch_settings(sb, oracle, tune, K, p, slots, pfd, waves, swz, rows):
+    tune(slots, pfd, waves, swz, rows)
     mesh = sb.build_mesh(K, p)
     op = sb.build_gather(mesh)
     q = d(np.random.default_rng([K, p, 72]).uniform(-1, 1, mesh.nl))
-    out = sweep(op.geometry, op.row_starts, op.col_ids, op.ng, op.nl, q)
-    assert np.array_equal(h(out), expect(oracle, op.row_starts, op.col_ids, q))
+    out = sweep(op.geometry, op.row_starts_dev, op.col_ids_dev, op.ng, op.nl, q)
+    assert np.array_equal(h(out), expect(oracle, op.row_starts_dev, op.col_ids_dev, q))
 
 
 @pytest.mark.parametrize("K,p,world", [(8, 1, 2), (9, 2, 3), (12, 1, 4), (40, 1, 3), (21, 2, 2)])
@@ -113,7 +113,7 @@ def test_sweep_slabs_with_carry(sb, oracle, K, p, world):
             carry = d(rng.uniform(-1, 1, part.plane)) if rank > 0 and op is ops[0] else None
             out = torch.empty(op.ng, dtype=torch.float64, device="cuda")
             bs6_gather_into(op, q, out, carry)
-            assert np.array_equal(h(out), expect(oracle, op.row_starts, op.col_ids, q, carry)), rank
+            assert np.array_equal(h(out), expect(oracle, op.row_starts_dev, op.col_ids_dev, q, carry)), rank
 
 
 def test_sweep_other_csr_same_rows(sb, oracle):
@@ -123,12 +123,12 @@ def test_sweep_other_csr_same_rows(sb, oracle):
     mesh = sb.build_mesh(K, p)
     op = sb.build_gather(mesh)
     rng = np.random.default_rng(74)
-    ci = h(op.col_ids)
+    ci = h(op.col_ids_dev)
     perm = rng.permutation(ci.shape[0]).astype(np.int32)
     q = d(rng.uniform(-1, 1, mesh.nl))
     ci2 = d(perm[ci])
-    out = sweep(op.geometry, op.row_starts, ci2, op.ng, op.nl, q)
-    assert np.array_equal(h(out), expect(oracle, op.row_starts, ci2, q))
+    out = sweep(op.geometry, op.row_starts_dev, ci2, op.ng, op.nl, q)
+    assert np.array_equal(h(out), expect(oracle, op.row_starts_dev, ci2, q))
 
 
 @pytest.mark.parametrize("p", [1, 2])
@@ -165,10 +165,10 @@ def test_sweep_odd_tails_and_offset_views(sb, oracle):
         base = torch.from_numpy(np.random.default_rng([K, 76]).uniform(-1, 1, mesh.nl + 1)).cuda()
         for q in (base[:mesh.nl].clone(), base[1:]):
             out = sb.bs6_gather(op, q)
-            assert np.array_equal(h(out), expect(oracle, op.row_starts, op.col_ids, q)), K
+            assert np.array_equal(h(out), expect(oracle, op.row_starts_dev, op.col_ids_dev, q)), K
         assert sweep_geometry(op, base[1:]) is None
         with pytest.raises(ValueError):
-            sweep(op.geometry, op.row_starts, op.col_ids, op.ng, op.nl, base[1:])
+            sweep(op.geometry, op.row_starts_dev, op.col_ids_dev, op.ng, op.nl, base[1:])
 
 
 def test_sweep_rejects_bad_geometry(sb):
@@ -182,7 +182,7 @@ def test_sweep_rejects_bad_geometry(sb):
                         ((4, 1, 2, 2, 0, 5), op.ng, op.nl),         # empty slab
                         ((4, 1, 0, 4, 3, 6), op.ng, op.nl)]:        # planes past the mesh
         with pytest.raises(ValueError):
-            sweep(geo, op.row_starts, op.col_ids, ng, nl, q)
+            sweep(geo, op.row_starts_dev, op.col_ids_dev, ng, nl, q)
     with pytest.raises(ValueError):
         _lib.check(_lib.lib().sb_bs6_sweep_tune(2, -1, 0, -1, 0), "tune")
 
@@ -204,7 +204,7 @@ def test_sweep_c3_full_size(sb, oracle, p):
         q = torch.empty(op.nl, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
         assert sweep_geometry(op, q) is not None
         out = h(sb.bs6_gather(op, q))
-        want = oracle.bs6_gather(h(op.row_starts), h(op.col_ids), h(q))
+        want = oracle.bs6_gather(h(op.row_starts_dev), h(op.col_ids_dev), h(q))
         assert np.array_equal(out, want)
     finally:
         oracle.set_threads(1)

@@ -49,11 +49,11 @@ def test_sequential_ranks_bitexact(sb, K, p, world):
         # BS7 over the rank's read window
         a, b = part.read_span(r)
         l2g = build_slab_l2g(K, p, z0, z1)
-        assert torch.equal(l2g, mesh.local_to_global[lo:hi])
+        assert torch.equal(l2g, mesh.local_to_global_dev[lo:hi])
         ids = l2g - a
         ql = torch.zeros(hi - lo, dtype=torch.float64, device="cuda")
         D._gpu_scatter(ids, qg[a:b].clone(), ql)
-        assert torch.equal(ql, qg[mesh.local_to_global[lo:hi].long()])
+        assert torch.equal(ql, qg[mesh.local_to_global_dev[lo:hi].long()])
 
 
 def test_nccl_one_rank_group(sb):
@@ -80,7 +80,7 @@ def test_nccl_one_rank_group(sb):
         sc.window.uniform_(-1, 1)
         ql = torch.zeros(mesh.nl, dtype=torch.float64, device=dev)
         sc.scatter(ql)
-        assert torch.equal(ql, sc.window[mesh.local_to_global.long()])
+        assert torch.equal(ql, sc.window[mesh.local_to_global_dev.long()])
     finally:
         dist.destroy_process_group()
 

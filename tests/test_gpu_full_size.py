@@ -57,12 +57,12 @@ def test_c5_mesh_gather_scatter_whole_on_one_gpu(sb):
     xg = torch.randint(-(1 << 20), 1 << 20, (mesh.ng,), generator=gen, device="cuda").to(torch.float64)
     ql = torch.empty(mesh.nl, dtype=torch.float64, device="cuda")
     sb.bs7_scatter(ids, xg, ql)
-    l2g = mesh.local_to_global
+    l2g = mesh.local_to_global_dev
     step = 100_000_000
     for a in range(0, mesh.nl, step):  # BS7 == plain indexing, chunk by chunk
         assert torch.equal(ql[a:a + step], xg[l2g[a:a + step].long()])
     op = sb.build_gather(mesh)
     del ids
     out = sb.bs6_gather(op, ql)
-    mult = sb.multiplicity(mesh)
+    mult = sb.mesh.multiplicity_dev(mesh)
     assert torch.equal(out, mult * xg)  # Z^T Z x = diag(Z^T 1) x, exact for integer x

@@ -62,10 +62,10 @@ def test_host_mesh_ops(sb):
     qg = rng.uniform(-1, 1, mesh.ng)
     ql = np.full(mesh.nl, 5.0)
     sb.bs7_scatter(ids, qg, ql)
-    assert np.array_equal(ql, qg[mesh.local_to_global.cpu().numpy()])
+    assert np.array_equal(ql, qg[mesh.local_to_global_dev.cpu().numpy()])
     masked = sb.build_scatter_ids(mesh, mask={0, 1, 2})
     ql2 = np.full(mesh.nl, 5.0)
     sb.bs7_scatter(masked, qg, ql2)
-    keep = masked.ids.cpu().numpy() >= 0
-    assert np.array_equal(ql2[keep], qg[mesh.local_to_global.cpu().numpy()][keep])
+    keep = masked.ids_dev.cpu().numpy() >= 0
+    assert np.array_equal(ql2[keep], qg[mesh.local_to_global_dev.cpu().numpy()][keep])
     assert (ql2[~keep] == 5.0).all()

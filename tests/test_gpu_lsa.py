@@ -111,7 +111,7 @@ def test_bs7_halo_through_lsa_window_bitexact(lsa, K, p, world):
     mesh = sb.build_mesh(K, p)
     gen = torch.Generator(device="cuda"); gen.manual_seed(3 * K + p)
     qg = torch.empty(mesh.ng, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
-    want = qg[mesh.local_to_global.long()]
+    want = qg[mesh.local_to_global_dev.long()]
     if not hasattr(lsa, "_halo_ok"):
         lsa.halo_window(2 * 8 * 4_000_000)
         lsa._halo_ok = True

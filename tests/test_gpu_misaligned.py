@@ -31,5 +31,5 @@ def test_offset_views_bitwise(sb, K, p):
         qg = gbase[off:off + mesh.ng]
         ql = torch.zeros(mesh.nl, dtype=torch.float64, device="cuda")
         sb.bs7_scatter(ids, qg, ql)
-        assert torch.equal(ql, qg[mesh.local_to_global.long()]), off
+        assert torch.equal(ql, qg[mesh.local_to_global_dev.long()]), off
     assert want6.shape[0] == mesh.ng
