@@ -116,6 +116,10 @@ int sb_bs6_gather(const int32_t *block_starts, int64_t n_blocks, const int32_t *
 int64_t sb_bs6_plan_size(int64_t n_blocks, int64_t nodes_per_block);
 int sb_bs6_make_plan(const int32_t *block_starts, int64_t n_blocks, const int32_t *row_starts,
                      int64_t nodes_per_block, int32_t *plan, sb_stream_t stream);
+/* Name of the kernel sb_bs6_gather_planned launches for this operator shape
+ * (written into name[cap]; tests and the bench report it). */
+int sb_bs6_planned_kernel(int64_t n_blocks, int64_t nodes_per_block, int64_t ng, int64_t nl,
+                          char *name, size_t cap);
 int sb_bs6_gather_planned(const int32_t *plan, int64_t n_blocks, int64_t nodes_per_block,
                           const int32_t *row_starts, const int32_t *col_ids, int64_t ng,
                           int64_t nl, const double *q_local, double *out,

@@ -22,6 +22,7 @@
 //
 // Results are bitwise those of the one-tile kernels: BS6 still sums each row
 // in ascending column order from +0.0 (or the carry-in) in one thread.
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -357,6 +358,48 @@ int bs6_rows_launch(const int32_t *rs, const int32_t *ci, int64_t ng, const doub
 
 static int64_t bs6_G(int64_t npb) { return std::max<int64_t>(1, kBs6Cap / npb); }
 
+// Kernel, value-tile swizzle and CTAs per SM of the planned gather, by the
+// mean row length rho = nl/ng (measured on B200 over N = 1..15,
+// profiles/r01_bs6_variants.md):
+//   rho >= 4    (p = 1)   pairs, swizzled, 1024-entry super-blocks (two plan
+//                         super-blocks each), 6 CTAs/SM (+3-6% over 512
+//                         entries at 12/SM) once the operator fills two waves
+//                         of them; else 512 entries, 12/SM
+//   rho >= 3    (p = 2)   lanes, plain,    12 CTAs/SM
+//   rho >= 2.2  (p = 3)   lanes, swizzled,  8 CTAs/SM (64 registers)
+//   rho <  2.2  (p >= 4)  lanes, plain,    10 CTAs/SM (48 registers)
+// SB200_BS6_CFG="<lanes|pairs|wide|rows>,<swizzle 0|1>,<CTAs/SM 6|8|10|12>"
+// overrides the choice (A/B runs, scripts/expt/time_bs6.py; read per call).
+struct Bs6Choice {
+    bool rows, pairs, sw, wide;
+    int mb;
+};
+static Bs6Choice bs6_choose(int64_t nsb, int64_t ng, int64_t nl) {
+    Bs6Choice c{false, false, false, false, 10};
+    if (nl >= 4 * ng) {
+        // wide only when every SM gets at least two of its super-blocks: on
+        // small operators half as many CTAs is a longer critical path
+        c.pairs = true; c.sw = true; c.mb = 12;
+        c.wide = nsb >= 2 * 2 * 6 * (int64_t)sm_count();
+    } else if (nl >= 3 * ng) {
+        c.mb = 12;
+    } else if (5 * nl >= 11 * ng) {
+        c.sw = true; c.mb = 8;
+    }
+    const char *cfg = getenv("SB200_BS6_CFG");
+    if (cfg && strncmp(cfg, "rows", 4) == 0) {
+        c.rows = true;
+    } else if (cfg) {
+        c.wide = cfg[0] == 'w';  // "wide": the 1024-entry pairs kernel
+        c.pairs = cfg[0] == 'p' || c.wide;
+        const char *c1 = strchr(cfg, ',');
+        c.sw = c1 && c1[1] == '1';
+        const char *c2 = c1 ? strchr(c1 + 1, ',') : nullptr;
+        c.mb = c2 ? atoi(c2 + 1) : 12;
+    }
+    return c;
+}
+
 // plans sb_bs6_make_plan found oversize (keyed by the plan's address; a new
 // plan built at the same address overwrites its entry)
 static std::mutex g_plan_mu;
@@ -401,6 +444,25 @@ int sb_bs6_make_plan(const int32_t *bst, int64_t nblk, const int32_t *rs, int64_
     return SB_OK;
 }
 
+int sb_bs6_planned_kernel(int64_t n_blocks, int64_t nodes_per_block, int64_t ng, int64_t nl, char *name,
+                          size_t cap) {
+    clear_error();
+    const int64_t psize = sb_bs6_plan_size(n_blocks, nodes_per_block);
+    if (psize == 0 || !name || cap == 0) {
+        set_error("sb_bs6_planned_kernel: invalid arguments");
+        return SB_E_INVALID;
+    }
+    const Bs6Choice c = bs6_choose(psize / 2 - 2, ng, nl);
+    if (c.rows)
+        snprintf(name, cap, "k_bs6_rows");
+    else if (c.wide)
+        snprintf(name, cap, "k_bs6_pairs<128,1024,%s,6,2>", c.sw ? "swz" : "plain");
+    else
+        snprintf(name, cap, "%s<128,512,%s,%d>", c.pairs ? "k_bs6_pairs" : "k_bs6_lanes", c.sw ? "swz" : "plain",
+                 c.mb);
+    return SB_OK;
+}
+
 int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const int32_t *rs,
                           const int32_t *ci, int64_t ng, int64_t nl, const double *q, double *out,
                           const double *carry, int64_t ncarry, sb_stream_t s) {
@@ -427,39 +489,10 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const 
     const size_t smem = 2 * kBs6Cap * sizeof(double);
     using KernT = void (*)(const int32_t *, int64_t, const int32_t *, const int32_t *, const double *, double *,
                            const double *, int64_t);
-    // Kernel, value-tile swizzle and CTAs per SM by the mean row length
-    // rho = nl/ng (measured on B200 over N = 1..15, profiles/r01_bs6_variants.md):
-    //   rho >= 4    (p = 1)   pairs, swizzled, 1024-entry super-blocks (two
-    //                         plan super-blocks each), 6 CTAs/SM (+3-6% over
-    //                         512 entries at 12/SM) once the operator fills
-    //                         two waves of them; else 512 entries, 12/SM
-    //   rho >= 3    (p = 2)   lanes, plain,    12 CTAs/SM
-    //   rho >= 2.2  (p = 3)   lanes, swizzled,  8 CTAs/SM (64 registers)
-    //   rho <  2.2  (p >= 4)  lanes, plain,    10 CTAs/SM (48 registers)
-    // SB200_BS6_CFG="<lanes|pairs|wide>,<swizzle 0|1>,<CTAs/SM 6|8|10|12>" overrides
-    // the choice (A/B runs, scripts/expt/time_bs6.py).
-    bool pairs, sw, wide = false;
-    int mb;
-    if (nl >= 4 * ng) {
-        // wide only when every SM gets at least two of its super-blocks: on
-        // small operators half as many CTAs is a longer critical path
-        pairs = true; sw = true; mb = 12;
-        wide = nsb >= 2 * 2 * 6 * (int64_t)sm_count();
-    }
-    else if (nl >= 3 * ng) { pairs = false; sw = false; mb = 12; }
-    else if (5 * nl >= 11 * ng) { pairs = false; sw = true; mb = 8; }
-    else { pairs = false; sw = false; mb = 10; }
-    const char *cfg = getenv("SB200_BS6_CFG");  // (per call: A/B runs and tests switch it)
-    if (cfg && cfg[0] == 'r' && cfg[1] == 'o' && cfg[2] == 'w' && cfg[3] == 's')
-        return bs6_rows_launch(rs, ci, ng, q, out, carry, ncarry, as_stream(s));
-    if (cfg) {
-        wide = cfg[0] == 'w';  // "wide": the 1024-entry pairs kernel
-        pairs = cfg[0] == 'p' || wide;
-        const char *c1 = strchr(cfg, ',');
-        sw = c1 && c1[1] == '1';
-        const char *c2 = c1 ? strchr(c1 + 1, ',') : nullptr;
-        mb = c2 ? atoi(c2 + 1) : 12;
-    }
+    Bs6Choice ch = bs6_choose(nsb, ng, nl);
+    if (ch.rows) return bs6_rows_launch(rs, ci, ng, q, out, carry, ncarry, as_stream(s));
+    const bool pairs = ch.pairs, sw = ch.sw, wide = ch.wide;
+    const int mb = ch.mb;
 #define SB_PICK(K_, MB_) (sw ? K_<T, kBs6Cap, true, MB_> : K_<T, kBs6Cap, false, MB_>)
 #define SB_PICK_MB(K_) (mb == 6 ? SB_PICK(K_, 6) : mb == 8 ? SB_PICK(K_, 8) : mb == 10 ? SB_PICK(K_, 10) : SB_PICK(K_, 12))
     auto grid_for = [&](const void *k) {

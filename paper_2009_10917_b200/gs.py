@@ -43,6 +43,20 @@ def sweep_geometry(op, q_local):
     return geo
 
 
+def bs6_kernel_name(op, q_local=None) -> str:
+    """Name of the kernel bs6_gather_into launches for `op` (tests, bench)."""
+    import ctypes
+    if q_local is not None and sweep_geometry(op, q_local) is not None:
+        return f"k_bs6_sweep<p={op.geometry[1]}>"
+    plan = op.plan() if hasattr(op, "plan") else None
+    if plan is None:
+        return "k_bs6 (unplanned)"
+    buf = ctypes.create_string_buffer(96)
+    _lib.check(_lib.lib().sb_bs6_planned_kernel(op.n_blocks, op.nodes_per_block, op.ng, op.nl, buf, 96),
+               "bs6_kernel_name")
+    return buf.value.decode()
+
+
 @_lib.device_guard
 def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) -> torch.Tensor:
     """Device-only BS6 writing `out` (length op.ng); optional carry-in partials

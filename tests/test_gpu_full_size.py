@@ -66,3 +66,38 @@ def test_c5_mesh_gather_scatter_whole_on_one_gpu(sb):
     out = sb.bs6_gather(op, ql)
     mult = sb.mesh.multiplicity_dev(mesh)
     assert torch.equal(out, mult * xg)  # Z^T Z x = diag(Z^T 1) x, exact for integer x
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 10, 15])
+def test_c3_gather_scatter_full_size_vs_oracle(sb, oracle, p):
+    """Config 3 (NG ~ 1e8 global DOFs) at order p through the public calls,
+    against the OpenMP oracle (oracle/sb_oracle.c restating gs.py:10-39) for
+    BS6 and plain indexing q_global[l2g] (harness.py:216-217) for BS7; at p = 1
+    (K = 463, NL = 7.9e8) the product path is the 1024-entry "wide" pairs
+    kernel, which the N = 7 bench point never runs."""
+    from paper_2009_10917_b200.gs import bs6_kernel_name
+    K = int(round((1e8 ** (1 / 3) - 1) / p))
+    mesh = sb.build_mesh(K, p)
+    op = sb.build_gather(mesh)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3000 + p)
+    q = torch.empty(op.nl, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
+    name = bs6_kernel_name(op, q)
+    if p == 1:
+        assert name.startswith("k_bs6_pairs<128,1024"), name
+    out = sb.bs6_gather(op, q)
+    oracle.set_threads(oracle.max_threads())
+    try:
+        want = oracle.bs6_gather(op.row_starts, op.col_ids, q.cpu().numpy())
+    finally:
+        oracle.set_threads(1)
+    assert np.array_equal(out.cpu().numpy(), want), name
+    del out, want
+    ids = sb.build_scatter_ids(mesh)
+    qg = torch.empty(mesh.ng, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
+    ql = torch.full((mesh.nl,), float("nan"), dtype=torch.float64, device="cuda")
+    sb.bs7_scatter(ids, qg, ql)
+    l2g = mesh.local_to_global_dev
+    step = 100_000_000
+    for a in range(0, mesh.nl, step):
+        assert torch.equal(ql[a:a + step], qg[l2g[a:a + step].long()])
