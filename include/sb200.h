@@ -125,6 +125,24 @@ int sb_bs6_gather_planned(const int32_t *plan, int64_t n_blocks, int64_t nodes_p
                           int64_t nl, const double *q_local, double *out,
                           const double *carry_in, int64_t n_carry, sb_stream_t stream);
 
+/* BS6 over a z-slab WITH its carry halo in one launch (multi-GPU, dist.py
+ * DistGather): the send operator's rows (this rank's top
+ * interface plane) are summed straight into rank r+1's carry buffer
+ * send_out[e & 1] (an NVLink-mapped address), the own operator's rows are
+ * seeded from carry[e & 1] for rows < n_carry once rank r-1's partials have
+ * landed.  `sync` (8 uint64, zeroed once, in this rank's symmetric window) holds
+ * [0] ready (written by rank r-1), [1] ack (written by rank r+1), [2] the call
+ * count e (device-side: CUDA-graph replays stay correct), [3..4] counters;
+ * peer_ready = rank r+1's sync[0], peer_ack = rank r-1's sync[1] (NULL at
+ * the ends; send_plan NULL on the last rank).  Plans from sb_bs6_make_plan
+ * with the same nodes_per_block.  Results bitwise sb_bs6_gather's. */
+int sb_bs6_gather_halo(const int32_t *send_plan, int64_t send_nblk, const int32_t *send_rs,
+                       const int32_t *send_ci, double *const send_out[2], const int32_t *own_plan,
+                       int64_t own_nblk, const int32_t *own_rs, const int32_t *own_ci, int64_t own_ng,
+                       double *own_out, const double *const carry[2], int64_t n_carry, int64_t npb,
+                       const double *q, uint64_t *sync, uint64_t *peer_ready, uint64_t *peer_ack,
+                       sb_stream_t stream);
+
 /* TMA-staged BS6 for structured operators of low order (p <= 2; the fast
  * path there).  A tile is ey*p x ez*p row lines (y, z) x w rows (x) of the
  * mesh.py:73-97 numbering; the producer warp of a persistent kernel copies the

@@ -405,6 +405,143 @@ static Bs6Choice bs6_choose(int64_t nsb, int64_t ng, int64_t nl) {
 static std::mutex g_plan_mu;
 static std::unordered_map<const int32_t *, bool> g_plan_oversize;
 
+// ---- BS6 + the multi-GPU carry halo in ONE launch ------
+// Rank r of a z-slab partition (dist.py DistGather) computes the partial sums
+// of its top interface plane (the "send" operator) and hands them to rank
+// r+1, which seeds those rows with them (carry) -- bitwise the 1-GPU gather
+// (SURVEY Appendix A.4).  Here both operators run in one persistent kernel:
+// virtual super-block v < nsb_send is a send super-block (its row sums are
+// stored straight into rank r+1's carry buffer, an NVLink-mapped address),
+// v >= nsb_send an own one; CTAs take v in increasing order, so every send
+// super-block is issued before any own one.  Protocol, all state in device
+// memory (so CUDA-graph replays stay correct; the host never tracks parity):
+//   sync[0] ready  -- written by rank r-1: its call e's carry is complete (e+1)
+//   sync[1] ack    -- written by rank r+1: it consumed call e's carry (e+1)
+//   sync[2] epoch  -- this rank's call count e (carry buffer e & 1)
+//   sync[3], [4]   -- CTA counters (send phase done, kernel done)
+// * before storing call e's partials into buffer e&1 of rank r+1: wait until
+//   ack >= e-1 (rank r+1 has consumed call e-2, the buffer's last user);
+// * the last CTA through the send phase publishes peer_ready = e+1 after a
+//   system-scope fence (every CTA fences its stores before counting);
+// * before reading carry rows: wait until ready >= e+1;
+// * the last CTA out stores peer_ack = e+1 into rank r-1 and advances epoch.
+// No wait depends on this rank's own later work, and every CTA is resident
+// (grid = occupancy x SMs), so the kernel cannot deadlock against itself.
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void wait_at_least(const uint64_t *flag, uint64_t v) {
+    while (ld_acquire_sys(flag) < v) __nanosleep(64);
+}
+
+struct Bs6HaloArgs {
+    const int32_t *plan[2];   // send, own
+    int64_t nsb[2];
+    const int32_t *rs[2], *ci[2];
+    double *send_out[2];      // rank r+1's carry buffers (NVLink-mapped), by epoch parity
+    double *own_out;
+    const double *carry[2];   // this rank's carry buffers (written by rank r-1)
+    int64_t ncarry;
+    const double *q;
+    uint64_t *sync;           // this rank's ready / ack / epoch / counters
+    uint64_t *peer_ready;     // rank r+1's sync[0] (NULL on the last rank)
+    uint64_t *peer_ack;       // rank r-1's sync[1] (NULL on the first rank)
+};
+
+template <int T, int CAP, bool SWZ, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_bs6_halo(Bs6HaloArgs A) {
+    constexpr int E = CAP / T;
+    extern __shared__ __align__(16) unsigned char bs6_smem[];
+    double(*qs)[CAP] = reinterpret_cast<double(*)[CAP]>(bs6_smem);
+    __shared__ uint64_t s_epoch;
+    if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile uint64_t *>(A.sync + 2);
+    __syncthreads();
+    const uint64_t epoch = s_epoch;
+    const int par = (int)(epoch & 1);
+    const int64_t g = gridDim.x, nsend = A.nsb[0], ntot = A.nsb[0] + A.nsb[1];
+    auto meta = [&](int64_t v) { return v < nsend ? load_meta(A.plan[0], v, nsend) : load_meta(A.plan[1], v - nsend, A.nsb[1]); };
+    bool send_counted = false, acked = false, readied = false;
+    auto count_send = [&]() {  // this CTA is past its last send super-block
+        __threadfence_system();  // every thread's stores into rank r+1's buffer
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long old = atomicAdd(reinterpret_cast<unsigned long long *>(A.sync + 3), 1ull);
+            if (old == (unsigned long long)(g - 1)) {
+                A.sync[3] = 0;
+                __threadfence_system();
+                if (A.peer_ready) st_release_sys(A.peer_ready, epoch + 1);
+            }
+        }
+        send_counted = true;
+    };
+    int64_t v = blockIdx.x;
+    int32_t col[E];
+    Bs6Rows<T, CAP> rw;
+    int buf = 0;
+    if (v < ntot) {
+        SbMeta mc = meta(v), mn = meta(v + g);
+        int side = v < nsend ? 0 : 1;
+        {
+            const int ne = mc.e1 - mc.e0;
+#pragma unroll
+            for (int j = 0; j < E; j++)
+                if ((int)threadIdx.x + j * T < ne) col[j] = ld_stream(A.ci[side] + mc.e0 + threadIdx.x + j * T);
+        }
+        for (; v < ntot; v += g) {
+            const int nside = v + g < nsend ? 0 : 1;
+            if (side == 1 && !send_counted) count_send();
+            const int ne = mc.e1 - mc.e0;
+            double vv[E];
+#pragma unroll
+            for (int j = 0; j < E; j++)
+                if ((int)threadIdx.x + j * T < ne) vv[j] = __ldg(A.q + col[j]);
+            bs6_load_rows<T, CAP>(mc, A.rs[side], rw);
+            const int nne = mn.e1 - mn.e0;
+#pragma unroll
+            for (int j = 0; j < E; j++)
+                if ((int)threadIdx.x + j * T < nne) col[j] = ld_stream(A.ci[nside] + mn.e0 + threadIdx.x + j * T);
+            const SbMeta mnn = meta(v + 2 * g);
+#pragma unroll
+            for (int j = 0; j < E; j++)
+                if ((int)threadIdx.x + j * T < ne) qs[buf][qslot<SWZ>(threadIdx.x + j * T)] = vv[j];
+            if (side == 0 && !acked) {  // rank r+1 is done with this buffer's previous contents
+                if (threadIdx.x == 0 && epoch >= 2) wait_at_least(A.sync + 1, epoch - 1);
+                acked = true;
+            }
+            const bool carry_rows = side == 1 && mc.r0 < A.ncarry;
+            if (carry_rows && !readied) {  // rank r-1's partials of this call have landed
+                if (threadIdx.x == 0) wait_at_least(A.sync + 0, epoch + 1);
+                readied = true;
+            }
+            __syncthreads();
+            if (side == 0)
+                bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], A.send_out[par], nullptr, 0);
+            else
+                bs6_row_sums<T, CAP, SWZ>(mc, rw, qs[buf], A.own_out, A.carry[par], carry_rows ? A.ncarry : 0);
+            buf ^= 1;
+            mc = mn;
+            mn = mnn;
+            side = nside;
+        }
+    }
+    if (!send_counted) count_send();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long old = atomicAdd(reinterpret_cast<unsigned long long *>(A.sync + 4), 1ull);
+        if (old == (unsigned long long)(g - 1)) {
+            A.sync[4] = 0;
+            A.sync[2] = epoch + 1;
+            __threadfence_system();
+            if (A.peer_ack) st_release_sys(A.peer_ack, epoch + 1);
+        }
+    }
+}
+
 }  // namespace sb
 
 using namespace sb;
@@ -461,6 +598,69 @@ int sb_bs6_planned_kernel(int64_t n_blocks, int64_t nodes_per_block, int64_t ng,
         snprintf(name, cap, "%s<128,512,%s,%d>", c.pairs ? "k_bs6_pairs" : "k_bs6_lanes", c.sw ? "swz" : "plain",
                  c.mb);
     return SB_OK;
+}
+
+int sb_bs6_gather_halo(const int32_t *send_plan, int64_t send_nblk, const int32_t *send_rs,
+                       const int32_t *send_ci, double *const send_out[2], const int32_t *own_plan,
+                       int64_t own_nblk, const int32_t *own_rs, const int32_t *own_ci, int64_t own_ng,
+                       double *own_out, const double *const carry[2], int64_t n_carry, int64_t npb,
+                       const double *q, uint64_t *sync, uint64_t *peer_ready, uint64_t *peer_ack,
+                       sb_stream_t s) {
+    clear_error();
+    const int64_t own_size = sb_bs6_plan_size(own_nblk, npb);
+    const bool has_send = send_plan != nullptr;
+    const int64_t send_size = has_send ? sb_bs6_plan_size(send_nblk, npb) : 0;
+    if (own_size == 0 || !own_plan || !own_rs || !own_ci || !own_out || !q || !sync || n_carry < 0 ||
+        (n_carry > 0 && (!carry || !carry[0] || !carry[1])) ||
+        (has_send && (send_size == 0 || !send_rs || !send_ci || !send_out || !send_out[0] || !send_out[1])) ||
+        (!has_send && peer_ready) || (n_carry == 0 && peer_ack)) {
+        set_error("sb_bs6_gather_halo: invalid arguments");
+        return SB_E_INVALID;
+    }
+    if ((reinterpret_cast<uintptr_t>(own_plan) | reinterpret_cast<uintptr_t>(send_plan) |
+         reinterpret_cast<uintptr_t>(sync)) & 7u) {
+        set_error("sb_bs6_gather_halo: plans and sync must be 8-byte aligned");
+        return SB_E_INVALID;
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        for (const int32_t *pl : {own_plan, send_plan}) {
+            const auto f = pl ? g_plan_oversize.find(pl) : g_plan_oversize.end();
+            if (f != g_plan_oversize.end() && f->second) {
+                set_error("sb_bs6_gather_halo: an operator's plan is oversize (use the unfused path)");
+                return SB_E_INVALID;
+            }
+        }
+    }
+    if (n_carry > own_ng) n_carry = own_ng;
+    Bs6HaloArgs A{};
+    A.plan[0] = send_plan;
+    A.plan[1] = own_plan;
+    A.nsb[0] = has_send ? send_size / 2 - 2 : 0;
+    A.nsb[1] = own_size / 2 - 2;
+    A.rs[0] = has_send ? send_rs : own_rs;
+    A.ci[0] = has_send ? send_ci : own_ci;
+    A.rs[1] = own_rs;
+    A.ci[1] = own_ci;
+    A.send_out[0] = has_send ? send_out[0] : nullptr;
+    A.send_out[1] = has_send ? send_out[1] : nullptr;
+    A.own_out = own_out;
+    A.carry[0] = n_carry ? carry[0] : nullptr;
+    A.carry[1] = n_carry ? carry[1] : nullptr;
+    A.ncarry = n_carry;
+    A.q = q;
+    A.sync = sync;
+    A.peer_ready = peer_ready;
+    A.peer_ack = peer_ack;
+    constexpr int T = kBs6T;
+    const size_t smem = 2 * kBs6Cap * sizeof(double);
+    // one kernel shape for both operators: lanes, 10 CTAs/SM (48 registers)
+    const auto k = k_bs6_halo<T, kBs6Cap, false, 10>;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k, T, smem);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(A.nsb[0] + A.nsb[1], (int64_t)sm_count() * std::max(1, per_sm)));
+    k<<<(unsigned)grid, T, smem, as_stream(s)>>>(A);
+    return launch_check("sb_bs6_gather_halo");
 }
 
 int sb_bs6_gather_planned(const int32_t *plan, int64_t nblk, int64_t npb, const int32_t *rs,

@@ -208,25 +208,29 @@ class DistGather:
                                                          nodes_per_block, device)
         return cls(part, rank, own, send, device, group=group)
 
-    def enable_lsa(self, lsa, offset: int = 0) -> None:
+    def enable_lsa(self, lsa, offset: int = 0, sync_offset: int | None = None) -> None:
         """Carry halo over NVLink peer memory (lsa.LsaReducer whose halo window
-        holds 2 planes at byte `offset`).  The send-plane gather then writes its
-        partials straight into rank+1's carry buffer (two buffers, alternating
-        per call) and one LSA barrier replaces the NCCL send/recv pair."""
+        holds 2 planes at byte `offset` and 8 zeroed uint64 sync words at
+        `sync_offset`).  gather_lsa then runs ONE kernel per call
+        (sb_bs6_gather_halo): the send plane's partials are stored straight
+        into rank+1's carry buffer (two buffers, by the device-side call
+        parity) and flag words in the windows replace the barrier."""
         nb = 8 * self.part.plane
-        self.lsa, self.epoch = lsa, 0
+        if sync_offset is None:
+            sync_offset = offset + 2 * nb
+        self.lsa = lsa
         self.carry_ptrs = [lsa.halo_pointers(offset + e * nb, self.rank)[0] for e in (0, 1)]
         self.send_ptrs = ([lsa.halo_pointers(offset + e * nb, self.rank + 1)[1] for e in (0, 1)]
                           if self.send_op is not None else None)
+        self.sync_ptr = lsa.halo_pointers(sync_offset, self.rank)[0]
+        self.peer_ready = (lsa.halo_pointers(sync_offset, self.rank + 1)[1]
+                           if self.send_op is not None else None)
+        self.peer_ack = lsa.halo_pointers(sync_offset + 8, self.rank - 1)[1] if self.rank > 0 else None
 
     def gather_lsa(self, q_slab: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
-        e = self.epoch
-        self.epoch ^= 1
-        if self.send_op is not None:
-            gather_raw(self.send_op, q_slab, self.send_ptrs[e], None, 0)
-        self.lsa.barrier()
-        gather_raw(self.own_op, q_slab, out.data_ptr(), self.carry_ptrs[e] if self.rank > 0 else None,
-                   self.part.plane if self.rank > 0 else 0)
+        gather_halo_raw(self.send_op, self.own_op, q_slab, out.data_ptr(), self.send_ptrs,
+                        self.carry_ptrs if self.rank > 0 else None, self.part.plane if self.rank > 0 else 0,
+                        self.sync_ptr, self.peer_ready, self.peer_ack)
         return out
 
     def exchange(self) -> None:
@@ -244,6 +248,30 @@ class DistGather:
         self.exchange()
         self.gather_fn(self.own_op, q_slab, out, self.carry)
         return out
+
+
+def gather_halo_raw(send_op, own_op, q: torch.Tensor, out_ptr: int, send_ptrs, carry_ptrs, ncarry: int,
+                    sync_ptr: int, peer_ready: int | None, peer_ack: int | None) -> None:
+    """sb_bs6_gather_halo: the send and own gathers of a slab plus the carry
+    handshake in one launch (raw addresses: NVLink-mapped peer memory, the
+    local halo window, or -- single-GPU emulation in the tests -- plain device
+    buffers)."""
+    import ctypes
+    L = _lib.lib()
+    own_plan = own_op.plan()
+    send_plan = send_op.plan() if send_op is not None else None
+    if own_plan is None or (send_op is not None and send_plan is None):
+        raise ValueError("the fused carry halo needs planned gather operators")
+    pair = ctypes.c_void_p * 2
+    so = pair(*send_ptrs) if send_ptrs else None
+    ca = pair(*carry_ptrs) if carry_ptrs else None
+    _lib.check(L.sb_bs6_gather_halo(
+        None if send_op is None else send_plan.data_ptr(), 0 if send_op is None else send_op.n_blocks,
+        None if send_op is None else send_op.row_starts_dev.data_ptr(),
+        None if send_op is None else send_op.col_ids_dev.data_ptr(), so,
+        own_plan.data_ptr(), own_op.n_blocks, own_op.row_starts_dev.data_ptr(), own_op.col_ids_dev.data_ptr(),
+        own_op.ng, out_ptr, ca, ncarry, own_op.nodes_per_block, q.data_ptr(), sync_ptr, peer_ready, peer_ack,
+        _lib.stream_handle(q.device)), "bs6_gather_halo")
 
 
 def gather_raw(op, q: torch.Tensor, out_ptr: int, carry_ptr: int | None, ncarry: int) -> None:
@@ -343,8 +371,8 @@ class DistMassOperator:
         self.scat = DistScatter.build(part, rank, device)
         self.gath = DistGather.build(part, rank, device)
         nb = 8 * part.plane
-        lsa.halo_window(4 * nb)  # [BS6 carry x2 | BS7 halo x2]
-        self.gath.enable_lsa(lsa, 0)
+        lsa.halo_window(4 * nb + 64)  # [BS6 carry x2 | BS7 halo x2 | BS6 sync words]
+        self.gath.enable_lsa(lsa, 0, sync_offset=4 * nb)
         self.scat.enable_lsa(lsa, 2 * nb)
         self.w = torch.as_tensor(weights, dtype=torch.float64).to(self.device)
         if self.w.shape[0] != part.nl(rank):
@@ -471,11 +499,12 @@ class BenchContext:
         self.scat = DistScatter.build(self.part, self.rank, device)
         if self.lsa is not None:
             nb = 8 * self.part.plane
-            self.lsa.halo_window(4 * nb)  # [BS6 carry x2 | BS7 halo x2]
-            self.gather.enable_lsa(self.lsa, 0)
+            self.lsa.halo_window(4 * nb + 64)  # [BS6 carry x2 | BS7 halo x2 | BS6 sync words]
+            self.gather.enable_lsa(self.lsa, 0, sync_offset=4 * nb)
             self.scat.enable_lsa(self.lsa, 2 * nb)
-            self.collective += ("; BS6 carry and BS7 halo planes written over NVLink into the peer's "
-                                "window + LSA barrier")
+            self.collective += ("; BS6 + carry halo in one launch (partials stored over NVLink into the "
+                                "peer's window, flag handshake); BS7 halo plane written over NVLink + LSA barrier")
+            self.launches_per_step = 7 + 2  # + BS7's halo put and LSA barrier (BS6 is one fused launch)
         return _SlabInfo(self.part, self.rank)
 
     def call(self, w, test):
