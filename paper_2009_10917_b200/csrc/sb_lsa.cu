@@ -161,7 +161,7 @@ int sb_lsa_create(const void *uid, size_t bytes, int nranks, int rank, sb_lsa_t 
             rc = SB_E_INVALID;
         }
     }
-    const size_t wbytes = 2 * kLsaMaxRanks * sizeof(double);
+    const size_t wbytes = kLsaWindowBytes;  // slots [2][kLsaMaxRanks] + the call counter
     if (!rc) rc = nccl_check(a.MemAlloc(&c->buf, wbytes), "ncclMemAlloc");
     if (!rc) rc = cuda_check(cudaMemset(c->buf, 0, wbytes), "sb_lsa_create memset");
     if (!rc) {
@@ -214,7 +214,7 @@ static LsaArgs lsa_args(sb_lsa_t *c) {
     LsaArgs L{};
     L.dc = c->dc;
     L.win = c->win;
-    L.epoch = (int)(c->calls++ & 1);
+    L.epoch = (int)(c->calls++ & 1);  // (informational; the kernels use the window's counter)
     L.enabled = 1;
     return L;
 }

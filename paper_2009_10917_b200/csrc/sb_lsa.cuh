@@ -10,7 +10,10 @@
 // path, with no collective launch, proxy thread or extra stream round trip.
 // Two slot sets (epoch = call parity) keep a fast rank's next call from
 // overwriting values a slow rank has not read yet: reaching call k+2 needs
-// every peer past call k+1's barrier, hence done reading call k.
+// every peer past call k+1's barrier, hence done reading call k.  The parity
+// comes from a call counter in this rank's window (kLsaCounterOff), read and
+// advanced by the combining thread -- never from the host, so a CUDA graph
+// that captured an odd number of calls still alternates across replays.
 #pragma once
 
 #include <nccl.h>
@@ -21,18 +24,24 @@
 namespace sb {
 
 constexpr int kLsaMaxRanks = 128;  // slots per epoch (NVLink domains up to NVL72)
+constexpr size_t kLsaCounterOff = 2 * kLsaMaxRanks * sizeof(double);  // uint64 call counter
+constexpr size_t kLsaWindowBytes = kLsaCounterOff + 64;
 
 struct LsaArgs {
     ncclDevComm dc;
     ncclWindow_t win;  // 2 x kLsaMaxRanks doubles, symmetric over the LSA team
-    int epoch;         // call parity
+    int epoch;         // (unused: the parity is device-side, kLsaCounterOff)
     int enabled;
 };
 
 // Thread 0 of the reduction's last CTA.
 __device__ __forceinline__ double lsa_combine(const LsaArgs &L, double v) {
     const ncclTeam lsa = ncclTeamLsa(L.dc);
-    const size_t base = (size_t)L.epoch * kLsaMaxRanks;
+    volatile unsigned long long *calls =
+        static_cast<volatile unsigned long long *>(ncclGetLocalPointer(L.win, kLsaCounterOff));
+    const unsigned long long call = *calls;
+    *calls = call + 1;  // (stream-ordered: the next combine runs in a later launch)
+    const size_t base = (size_t)(call & 1) * kLsaMaxRanks;
     for (int p = 0; p < lsa.nRanks; p++) {
         double *dst = static_cast<double *>(ncclGetLsaPointer(L.win, sizeof(double) * (base + lsa.rank), p));
         *reinterpret_cast<volatile double *>(dst) = v;

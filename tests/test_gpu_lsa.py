@@ -197,3 +197,26 @@ def test_abort_is_local_and_leaves_the_device_usable():
     import paper_2009_10917_b200 as sb
     assert r2.bs3_norm2(x) == 0.0 + sb.bs3_norm2(x)
     r2.close()
+
+
+def test_lsa_parity_is_device_side_across_graph_replays(lsa):
+    """An odd number of fused reductions captured in a CUDA graph: the slot
+    parity comes from the window's call counter, so replays keep alternating
+    and every result still equals the plain rank-order sum."""
+    import paper_2009_10917_b200 as sb
+    x = _v(100_003, 5)
+    want = 0.0 + sb.bs3_norm2(x)
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    lsa.bs3_norm2(x, out=out)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        for _ in range(3):
+            lsa.bs3_norm2(x, out=out)
+    torch.cuda.current_stream().wait_stream(side)
+    for _ in range(3):
+        g.replay()
+        torch.cuda.synchronize()
+        assert float(out.item()) == want
