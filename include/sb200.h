@@ -188,9 +188,20 @@ int sb_bs6_gather_sweep(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_
                         const int32_t *row_starts, const int32_t *col_ids, int64_t ng, int64_t nl,
                         const double *q_local, double *out, const double *carry_in, int64_t n_carry,
                         sb_stream_t stream);
+/* Row-line-tiled BS6 for structured operators of order p = 1 (the fast path
+ * there; csrc/sb_gs_tile.cu).  Same operator geometry contract as
+ * sb_bs6_gather_sweep.  A CTA takes <= 128 consecutive rows of one lattice
+ * row line and loads q in structure order (one 16 B node pair per element
+ * and run); those values are used only when the tile's row starts and column
+ * ids equal the closed form, otherwise the same kernel gathers in CSR order,
+ * so ANY CSR with these rows gives sb_bs6_gather's result bit for bit. */
+int sb_bs6_gather_tiled(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_lo, int32_t c_hi,
+                        const int32_t *row_starts, const int32_t *col_ids, int64_t ng, int64_t nl,
+                        const double *q_local, double *out, const double *carry_in, int64_t n_carry,
+                        sb_stream_t stream);
 /* Process-wide knobs of sb_bs6_gather_sweep for A/B runs (not thread-safe;
  * 0 / -1 restore the measured defaults): shared-memory ring slots (3..8,
- * default 4), L2 prefetch distance in element planes (-1: 4; 0: off), work
+ * default 4), L2 prefetch distance in element planes (-1: 0 = off; measured slower), work
  * items per resident CTA (default 8), value-tile swizzle (-1: for p = 1),
  * row lines per column = consumer warps per CTA (7, 8 or 16; 0: 8). */
 int sb_bs6_sweep_tune(int32_t slots, int32_t l2_prefetch_planes, int32_t waves, int32_t swizzle,

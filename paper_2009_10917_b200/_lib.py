@@ -107,6 +107,8 @@ _SIGS = {
     "sb_bs6_gather_halo": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_vp, _c_vp, _c_i64,
                                     _c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp]),
     "sb_bs6_planned_kernel": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_vp, _c_size]),
+    "sb_bs6_gather_tiled": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_vp, _c_vp, _c_i64,
+                                     _c_i64, _c_vp, _c_vp, _c_vp, _c_i64, _c_vp]),
     "sb_bs6_sweep_tune": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int]),
     "sb_bs6_make_plan": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_vp]),
     "sb_bs6_gather_planned": (_c_int, [_c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp,

@@ -15,6 +15,7 @@ void clear_error();
 
 inline int cuda_check(cudaError_t e, const char *what) {
     if (e != cudaSuccess) {
+        (void)cudaGetLastError();  // a reported (non-sticky) error must not resurface at the next launch check
         set_error("%s: %s", what, cudaGetErrorString(e));
         return SB_E_CUDA;
     }

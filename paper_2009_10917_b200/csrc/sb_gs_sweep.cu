@@ -161,23 +161,34 @@ struct SwCursor {
     }
 };
 
-// lane l < n: row start of row r0 + l; every lane: the end of the last row
-__device__ __forceinline__ void sw_load_rs(const SwRows &R, const int32_t *__restrict__ rs, int lane, int &lo,
-                                           int &end) {
+// Row starts of a warp-step go into the warp's ring of kSwRsSlots slots
+// with cp.async (LDGSTS: no register waits on the load), issued three steps
+// ahead: slot[l] = row start of row r0 + l (l < n; the end for l >= n),
+// slot[32] = the end of the last row.  Every step commits one group.
+constexpr int kSwRsSlots = 8, kSwRsStride = 40;
+
+__device__ __forceinline__ void sw_issue_rs(const SwRows &R, const int32_t *__restrict__ rs, int lane, int *slot) {
     if (R.n > 0) {
-        // lanes >= n load the end too (same address): no select on a load result
-        end = __ldg(rs + R.r0 + R.n);
-        lo = ld_stream(rs + R.r0 + (lane < R.n ? lane : R.n));
+        cp_async4(slot + lane, rs + R.r0 + (lane < R.n ? lane : R.n));
+        if (lane == 0) cp_async4(slot + 32, rs + R.r0 + R.n);
     } else {
-        lo = end = 0;
+        slot[lane] = 0;
+        if (lane == 0) slot[32] = 0;
     }
+    cp_async_commit();
+}
+
+// L2 prefetch of a warp-step's column indices (<= 8 lines of 128 B)
+__device__ __forceinline__ void sw_prefetch_cols(const int *slot, const int32_t *__restrict__ ci, int lane) {
+    const int e0 = slot[0], ne = slot[32] - e0;
+    if (lane * 32 < ne) asm volatile("prefetch.global.L2 [%0];" ::"l"(ci + e0 + lane * 32));
 }
 
 template <int E>
-__device__ __forceinline__ void sw_load_cols(int lo, int end, const int32_t *__restrict__ ci, int lane,
+__device__ __forceinline__ void sw_load_cols(const int *slot, const int32_t *__restrict__ ci, int lane,
                                              int (&col)[E]) {
-    const int e0 = __shfl_sync(0xffffffffu, lo, 0);
-    const int ne = end - e0;
+    const int e0 = slot[0];
+    const int ne = slot[32] - e0;
 #pragma unroll
     for (int j = 0; j < E; j++)
         if (lane + 32 * j < ne) col[j] = ld_stream(ci + e0 + lane + 32 * j);
@@ -194,26 +205,32 @@ struct SwState {
     int waited, wslot;   // planes waited for (count), next slot to wait on
     uint32_t wph;        // its phase
     int released, rslot; // planes released (count), next slot to release
+    int step;            // warp-steps done (row-start ring slot)
 };
 
-// One step (row plane c of the current item) of consumer warp `warp`.  colA /
-// loA / endA hold this step's column indices (loaded one step ago) and row
-// starts (two steps ago); colB is filled for the next step from loB / endB
-// (loaded one step ago), and loA / endA are refilled for the step after that
-// -- the two register sets alternate between calls, so no load result is
-// moved (and waited for) before the step that uses it.  Returns false after
-// the CTA's last step.
+// One step (row plane c of the current item) of consumer warp `warp`.  Row
+// starts arrive in the warp's smem ring four steps ahead (cp.async), the
+// column indices of step + 2 are prefetched into L2 and those of step + 1
+// loaded into colB; colA holds this step's (loaded one step ago).  colA /
+// colB alternate between calls, so no load result is moved (and waited for)
+// before the step that uses it.  Returns false after the CTA's last step.
 template <int P, int H, bool SWZ, int E>
 __device__ __forceinline__ bool sw_step(const SwGeom &G, SwState<P, H> &S, SwCursor<P, H> &ahead, int warp,
-                                        int lane, int (&colA)[E], int (&colB)[E], int &loA, int &endA, int &loB,
-                                        int &endB, const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
+                                        int lane, int (&colA)[E], int (&colB)[E], int *rsr,
+                                        const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
                                         const double *__restrict__ q, double *__restrict__ out,
                                         const double *__restrict__ carry, int64_t ncarry, uint64_t *full,
                                         uint64_t *empty, const double *ring, double *vt) {
-    const int lo0 = loA, end0 = endA;
-    sw_load_rs(ahead.rows(G), rs, lane, loA, endA);  // step + 2
+    const int st = S.step;
+    sw_issue_rs(ahead.rows(G), rs, lane, rsr + ((st + 4) & (kSwRsSlots - 1)) * kSwRsStride);  // step + 4
     ahead.next(G, warp);
-    sw_load_cols<E>(loB, endB, ci, lane, colB);  // step + 1
+    cp_async_wait<2>();  // row starts of steps + 1 and + 2 have landed (own copies) ...
+    __syncwarp();        // ... and the other lanes' too
+    sw_load_cols<E>(rsr + ((st + 1) & (kSwRsSlots - 1)) * kSwRsStride, ci, lane, colB);  // step + 1
+    sw_prefetch_cols(rsr + ((st + 2) & (kSwRsSlots - 1)) * kSwRsStride, ci, lane);       // step + 2
+    const int *cur = rsr + (st & (kSwRsSlots - 1)) * kSwRsStride;
+    const int lo0 = cur[lane], end0 = cur[32];
+    S.step = st + 1;
 
     const SwItem &I = S.I;
     const int c = S.c;
@@ -261,24 +278,58 @@ __device__ __forceinline__ bool sw_step(const SwGeom &G, SwState<P, H> &S, SwCur
             dd[1] = s0 + G.rs_d + (cb[1] & 1) - cb[1];
             dd[2] = s2 + (cb[2] & 1) - cb[2];
             dd[3] = s2 + G.rs_d + (cb[3] & 1) - cb[3];
-            bool fast = false;
+            // 0: generic run search; 1: interior fast path; 2: x-edge / partial fast path
+            int fast = 0;
             if constexpr (P == 1) {
-                // A structured interior warp-step -- 32 rows of 8 entries each
-                // in the closed-form order (mesh.py:113-134: element (a-1+dx,
-                // b-1+dy, c-1+dz), node (1-dx, 1-dy, 1-dz), entry dz*4+dy*2+dx)
-                // -- is verified against the loaded row starts and columns
-                // (one compare per entry) and then needs no run search: entry
-                // lane + 32 j has run (lane & 7) >> 1 for every j.
-                if (nrows == kSwW && z2 && y2 && I.a0 >= 1 && I.a0 + kSwW <= G.g - 1 && ne == kSwVt) {
-                    const int X = c00 + 7 + 8 * (lane >> 3) + ((lane >> 2) & 1) * (zstride - 4) +
-                                  ((lane >> 1) & 1) * (ystride - 2) + (lane & 1) * 7;
-                    bool ok = lo0 == e0 + 8 * lane;
+                // A structured warp-step -- rows in the closed-form order
+                // (mesh.py:113-134: entry j = dz*4 + dy*2 + dx of row a is node
+                // (1-dx, 1-dy, 1-dz) of element (a-1+dx, b-1+dy, c-1+dz)) -- is
+                // verified against the loaded row starts and columns (one
+                // compare per entry) and then needs no run search: entry
+                // lane + 32 J has run (lane & 7) >> 1 for every J.  Interior
+                // row lines only (both element rows in y and z present); the
+                // x-edge rows a = 0 (entries dx = 1) and a = g-1 (dx = 0) have
+                // 4 entries and shift the pattern (mode 2).
+                if (z2 && y2 && ne <= kSwVt) {
+                    // column of entry j = 0 of row a0 (element a0-1, node 7)
+                    const int B0 = c00 + 8 * (I.a0 - 1 - I.xlo) + 7;
+                    const int offl = ((lane >> 2) & 1) * (zstride - 4) + ((lane >> 1) & 1) * (ystride - 2) + (lane & 1) * 7;
+                    if (nrows == kSwW && I.a0 >= 1 && I.a0 + kSwW <= G.g - 1 && ne == kSwVt) {
+                        const int X = B0 + 8 * (lane >> 3) + offl;
+                        bool ok = lo0 == e0 + 8 * lane;
 #pragma unroll
-                    for (int j = 0; j < E; j++) ok = ok && colA[j] == X + 32 * j;
-                    fast = __all_sync(0xffffffffu, ok);
+                        for (int j = 0; j < E; j++) ok = ok && colA[j] == X + 32 * j;
+                        fast = __all_sync(0xffffffffu, ok) ? 1 : 0;
+                    } else {
+                        const bool first = I.a0 == 0, last = I.a0 + nrows == G.g;
+                        const int s0 = first ? 4 : 0, r1 = first ? 1 : 0;
+                        const int nfull = nrows - r1 - (last ? 1 : 0);
+                        const int ne_exp = s0 + 8 * nfull + (last ? 4 : 0);
+                        bool ok = ne == ne_exp && nfull >= 0;
+                        if (lane < nrows)
+                            ok = ok && lo0 == (lane == 0 && first ? e0 : e0 + s0 + 8 * (lane - r1));
+                        const int jl = (lane - s0) & 7;
+                        const int X = B0 + 8 * (r1 + ((lane - s0) >> 3)) +
+                                      ((jl >> 2) & 1) * (zstride - 4) + ((jl >> 1) & 1) * (ystride - 2) + (jl & 1) * 7;
+#pragma unroll
+                        for (int j = 0; j < E; j++) {
+                            const int k = lane + 32 * j, kp = k - s0;
+                            int want = X + 32 * j;
+                            if (kp < 0) {  // row 0: entries dx = 1, j = 2k + 1
+                                const int jj = 2 * k + 1;
+                                want = B0 + ((jj >> 2) & 1) * (zstride - 4) + ((jj >> 1) & 1) * (ystride - 2) + 7;
+                            } else if (kp >= 8 * nfull) {  // row g-1: entries dx = 0, j = 2m
+                                const int jj = 2 * (kp - 8 * nfull);
+                                want = B0 + 8 * (r1 + nfull) + ((jj >> 2) & 1) * (zstride - 4) +
+                                       ((jj >> 1) & 1) * (ystride - 2);
+                            }
+                            ok = ok && (k >= ne || colA[j] == want);
+                        }
+                        fast = __all_sync(0xffffffffu, ok) ? 2 : 0;
+                    }
                 }
             }
-            if (fast) {
+            if (fast == 1) {
                 const int D = (lane & 4) ? ((lane & 2) ? dd[3] : dd[2]) : ((lane & 2) ? dd[1] : dd[0]);
 #pragma unroll
                 for (int j = 0; j < E; j++) vt[vslot<SWZ>(lane + 32 * j)] = ring[colA[j] + D];
@@ -286,6 +337,28 @@ __device__ __forceinline__ bool sw_step(const SwGeom &G, SwState<P, H> &S, SwCur
 #pragma unroll
                 for (int t = 0; t < 8; t++) acc = add(acc, vt[vslot<SWZ>(8 * lane + t)]);
                 st_stream(out + r, acc);
+                __syncwarp();
+            } else if (fast == 2) {
+                // verified: every entry's run is its j >> 1 (rows 0 / g-1: 2k+1 / 2m)
+                const bool first = I.a0 == 0, last = I.a0 + nrows == G.g;
+                const int s0 = first ? 4 : 0, nfull = nrows - (first ? 1 : 0) - (last ? 1 : 0);
+                const int jl = (lane - s0) & 7;
+#pragma unroll
+                for (int j = 0; j < E; j++) {
+                    const int k = lane + 32 * j, kp = k - s0;
+                    const int run = kp < 0 ? k : (kp >= 8 * nfull ? kp - 8 * nfull : jl >> 1);
+                    const int D = (run & 2) ? ((run & 1) ? dd[3] : dd[2]) : ((run & 1) ? dd[1] : dd[0]);
+                    if (k < ne) vt[vslot<SWZ>(k)] = ring[colA[j] + D];
+                }
+                __syncwarp();
+                const int t0 = lane < nrows ? lo0 - e0 : 0, n = lane < nrows ? nxt - lo0 : 0;
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    const double v = vt[vslot<SWZ>((t0 + t) & (kSwVt - 1))];
+                    const double sum = add(acc, v);
+                    acc = t < n ? sum : acc;
+                }
+                if (lane < nrows) st_stream(out + r, acc);
                 __syncwarp();
             } else {
             // branch-free except for columns outside the runs (a warp vote)
@@ -451,19 +524,24 @@ __global__ void __launch_bounds__((H + 1) * 32, MB)
     S.c = S.I.c0;
     S.base = S.waited = S.wslot = S.released = S.rslot = 0;
     S.wph = 0;
-    SwCursor<P, H> ahead;  // two steps ahead of S
+    S.step = 0;
+    int *rsr = reinterpret_cast<int *>(ring + (size_t)nslot * G.plane_d + (size_t)H * kSwVt) +
+               warp * kSwRsSlots * kSwRsStride;
+    SwCursor<P, H> ahead;  // four steps ahead of S
     ahead.set(G, S.it, warp);
-    int lo0, end0, lo1, end1;
-    sw_load_rs(ahead.rows(G), rs, lane, lo0, end0);
-    ahead.next(G, warp);
-    sw_load_rs(ahead.rows(G), rs, lane, lo1, end1);
-    ahead.next(G, warp);
+    for (int k = 0; k < 4; k++) {
+        sw_issue_rs(ahead.rows(G), rs, lane, rsr + k * kSwRsStride);
+        ahead.next(G, warp);
+    }
+    cp_async_wait<0>();
+    __syncwarp();
     int col0[E], col1[E];
-    sw_load_cols<E>(lo0, end0, ci, lane, col0);
-    while (sw_step<P, H, SWZ, E>(G, S, ahead, warp, lane, col0, col1, lo0, end0, lo1, end1, rs, ci, q, out,
-                                 carry, ncarry, full, empty, ring, vt) &&
-           sw_step<P, H, SWZ, E>(G, S, ahead, warp, lane, col1, col0, lo1, end1, lo0, end0, rs, ci, q, out,
-                                 carry, ncarry, full, empty, ring, vt)) {
+    sw_load_cols<E>(rsr, ci, lane, col0);
+    sw_prefetch_cols(rsr + kSwRsStride, ci, lane);
+    while (sw_step<P, H, SWZ, E>(G, S, ahead, warp, lane, col0, col1, rsr, rs, ci, q, out, carry, ncarry, full,
+                                 empty, ring, vt) &&
+           sw_step<P, H, SWZ, E>(G, S, ahead, warp, lane, col1, col0, rsr, rs, ci, q, out, carry, ncarry, full,
+                                 empty, ring, vt)) {
     }
 }
 
@@ -479,7 +557,11 @@ int sweep_launch(const SwGeom &G0, const int32_t *rs, const int32_t *ci, const d
     const int nx_max = (kSwW - 1) / P + 2, ny_max = (H - 1) / P + 2;
     G.rs_d = (nx_max * N3 + 2 + 15) / 16 * 16;  // + the odd-start shift and 16 B rounding
     G.plane_d = ny_max * G.rs_d;
-    const size_t smem = kSwHdr + (size_t)G.nslot * G.plane_d * 8 + (size_t)H * kSwVt * 8;
+    auto smem_for = [&](int ns) {
+        return kSwHdr + (size_t)ns * G.plane_d * 8 + (size_t)H * kSwVt * 8 + (size_t)H * kSwRsSlots * kSwRsStride * 4;
+    };
+    while (G.nslot > 3 && smem_for(G.nslot) > 227 * 1024) G.nslot--;  // large columns: a shallower ring
+    const size_t smem = smem_for(G.nslot);
     using KernT = void (*)(SwGeom, const int32_t *, const int32_t *, const double *, double *, const double *,
                            int64_t);
     const KernT k = swz ? k_bs6_sweep<P, H, true, MB> : k_bs6_sweep<P, H, false, MB>;
@@ -542,7 +624,7 @@ int sb_bs6_gather_sweep(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_
     G.na = (int)((g + kSwW - 1) / kSwW);
     G.nl = nl;
     G.nslot = g_sw_slots > 0 ? g_sw_slots : 4;
-    G.pfd = g_sw_pfd >= 0 ? g_sw_pfd : 4;
+    G.pfd = g_sw_pfd >= 0 ? g_sw_pfd : 0;  // L2 prefetch measured slower (profiles/r02_bs6_sweep.md)
     const bool swz = g_sw_swz >= 0 ? g_sw_swz == 1 : p == 1;
     const cudaStream_t st = as_stream(stream);
     // row lines per column (one consumer warp each) and CTAs per SM: 8 / 2 by

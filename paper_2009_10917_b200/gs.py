@@ -46,6 +46,8 @@ def sweep_geometry(op, q_local):
 def bs6_kernel_name(op, q_local=None) -> str:
     """Name of the kernel bs6_gather_into launches for `op` (tests, bench)."""
     import ctypes
+    if q_local is not None and tiled_geometry(op, q_local) is not None:
+        return "k_bs6_tile1<128>"
     if q_local is not None and sweep_geometry(op, q_local) is not None:
         return f"k_bs6_sweep<p={op.geometry[1]}>"
     plan = op.plan() if hasattr(op, "plan") else None
@@ -57,6 +59,18 @@ def bs6_kernel_name(op, q_local=None) -> str:
     return buf.value.decode()
 
 
+def tiled_geometry(op, q_local):
+    """(K, p, z0, z1, c_lo, c_hi) when the row-line-tiled kernel
+    (csrc/sb_gs_tile.cu) takes this gather: a structured device operator of
+    order 1.  Opt-in (SB200_BS6_TILED=1) while it measures slower than the
+    super-block kernel (profiles/r02_bs6_sweep.md)."""
+    geo = getattr(op, "geometry", None)
+    if (geo is None or geo[1] != 1 or os.environ.get("SB200_BS6_TILED", "0") != "1"
+            or q_local.data_ptr() % 16):
+        return None
+    return geo
+
+
 @_lib.device_guard
 def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) -> torch.Tensor:
     """Device-only BS6 writing `out` (length op.ng); optional carry-in partials
@@ -64,6 +78,13 @@ def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) ->
     dev = q_local.device
     L = _lib.lib()
     ncarry = 0 if carry is None else int(carry.shape[0])
+    geo = tiled_geometry(op, q_local)
+    if geo is not None:
+        _lib.check(L.sb_bs6_gather_tiled(*geo, op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(), op.ng,
+                                         int(q_local.shape[0]), q_local.data_ptr(), out.data_ptr(),
+                                         None if carry is None else carry.data_ptr(), ncarry,
+                                         _lib.stream_handle(dev)), "bs6_gather")
+        return out
     geo = sweep_geometry(op, q_local)
     if geo is not None:
         _lib.check(L.sb_bs6_gather_sweep(*geo, op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(), op.ng,

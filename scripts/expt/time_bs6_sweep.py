@@ -70,6 +70,19 @@ def main():
             print(f"N={p:2d} K={K} sweep {cfg:>16s}  {ms:.3f} ms {nb / ms / 1e6:7.0f} GB/s  bitwise={ok}",
                   flush=True)
         _lib.check(L.sb_bs6_sweep_tune(0, -1, 0, -1, 0), "tune")
+        if p == 1:
+            def tiled():
+                rc = L.sb_bs6_gather_tiled(*op.geometry, op.row_starts_dev.data_ptr(), op.col_ids_dev.data_ptr(),
+                                           op.ng, op.nl, q.data_ptr(), out.data_ptr(), None, 0, st)
+                if rc:
+                    raise RuntimeError(_lib.last_error())
+            out.fill_(float("nan"))
+            tiled()
+            torch.cuda.synchronize()
+            ok = torch.equal(out, ref)
+            ms = timed(tiled)
+            print(f"N={p:2d} K={K} tiled                   {ms:.3f} ms {nb / ms / 1e6:7.0f} GB/s  bitwise={ok}",
+                  flush=True)
 
 
 if __name__ == "__main__":
