@@ -37,8 +37,52 @@ def to_bytes(v, unit):
     return float(v) * scale
 
 
+def bs6_section(specs):
+    """Extra rows: the BS6 product kernel at config 3's N=1/2 (scripts/profile_bs6_low.py)."""
+    from paper_2009_10917_b200.core import bytes_moved
+    out = ["", "BS6 at config 3's low orders (NG ~ 1e8; scripts/profile_bs6_low.py, the product path):", "",
+           "| N | kernel | duration us | DRAM read GB | DRAM write GB | traffic / algorithmic | achieved GB/s "
+           "(algorithmic) | DRAM % peak | L1 % peak | issue active % | regs | achieved occ % | top stalls |",
+           "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    for spec in specs:
+        rep, p = spec.rsplit(":", 1)
+        p = int(p)
+        K = int(round((1e8 ** (1 / 3) - 1) / p))
+        ng, nl = (K * p + 1) ** 3, K ** 3 * (p + 1) ** 3
+        algo = bytes_moved("bs6", nl=nl, ng=ng)
+        hdr, units, rows = raw(rep)
+        col = {h: i for i, h in enumerate(hdr)}
+        r = rows[-1]
+
+        def get(name):
+            i = col.get(name)
+            return (r[i], units[i]) if i is not None else ("", "")
+        dur_v, dur_u = get("gpu__time_duration.sum")
+        dur_us = float(dur_v) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(dur_u, 1.0)
+        rd = to_bytes(*get("dram__bytes_read.sum"))
+        wr = to_bytes(*get("dram__bytes_write.sum"))
+        stalls = []
+        for h, i in col.items():
+            if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
+                try:
+                    stalls.append((float(r[i]), h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        stalls.sort(reverse=True)
+        out.append(f"| {p} | `{get('Kernel Name')[0].split('(')[0]}` | {dur_us:.1f} | {rd / 1e9:.3f} | {wr / 1e9:.3f} | "
+                   f"{(rd + wr) / algo:.3f} | {algo / (dur_us * 1e-6) / 1e9:.0f} | "
+                   f"{float(get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')[0]):.1f} | "
+                   f"{float(get('l1tex__throughput.avg.pct_of_peak_sustained_active')[0] or 'nan'):.1f} | "
+                   f"{float(get('smsp__issue_active.avg.pct_of_peak_sustained_active')[0] or 'nan'):.1f} | "
+                   f"{get('launch__registers_per_thread')[0]} | "
+                   f"{float(get('sm__warps_active.avg.pct_of_peak_sustained_active')[0]):.1f} | "
+                   + ", ".join(f"{s} {v:.1f}" for v, s in stalls[:3]) + " |")
+    return out
+
+
 def main():
     rep, tag = sys.argv[1], sys.argv[2]
+    extra = [sys.argv[i + 1] for i, a in enumerate(sys.argv) if a == "--bs6"]
     from paper_2009_10917_b200.core import bytes_moved
     n = 100_000_000
     nl, ng = 147197952, 99252847  # K=66, N=7
@@ -85,7 +129,7 @@ def main():
         r = picked[t]
         name = get(r, "Kernel Name")[0].split("(")[0]
         dur_v, dur_u = get(r, "gpu__time_duration.sum")
-        dur_us = float(dur_v) / (1e3 if dur_u == "nsecond" else 1) if dur_u != "usecond" else float(dur_v)
+        dur_us = float(dur_v) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(dur_u, 1.0)
         rd = to_bytes(*get(r, "dram__bytes_read.sum"))
         wr = to_bytes(*get(r, "dram__bytes_write.sum"))
         pct = get(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")[0]
@@ -107,6 +151,8 @@ def main():
                      f"{(rd + wr) / algo[t]:.3f} | {ach:.0f} | {float(pct):.1f} | {float(l1):.1f} | {float(iss):.1f} | {regs} | "
                      f"{float(occ):.1f} | {top} |")
         traffic[KEYS[t]] = int(rd + wr)
+    if extra:
+        lines += bs6_section(extra)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
