@@ -23,6 +23,7 @@
 // gather in the same kernel, so results are right for ANY CSR with these
 // rows.  Row sums: the value tile + one thread per row, as in sb_gs_pipe.cu.
 #include <limits.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -256,6 +257,267 @@ __global__ void __launch_bounds__(kTlT, MINB)
     }
 }
 
+// ---- 32 x 4 tiles: four row lines per CTA (one per warp) ------------------
+// Element (ex, ey, ez)'s 64 B are two 32 B sectors, one per k (z) half; each
+// sector holds the four (j, i) nodes of that half, j (y) = 0 / 1 going to row
+// lines ey / ey+1.  A tile of 4 consecutive row lines b0..b0+3 at plane c
+// therefore reads the k = 1 half of plane c-1 and the k = 0 half of plane c
+// of element rows ey = b0-1 .. b0+3, and uses the inner three of those rows'
+// sectors completely (the one-row tiles above used every sector half, so L2
+// delivered 2x the useful bytes).  Staging plane pl = dz*8 + 2*ey3 + jn - 1
+// (ey3 = ey - (b0-1); edge rows hold one j half) keeps element e's node pair
+// at 2e: warp w (row line b0+w) reads entry j of row a0+lane at plane
+// dz*8 + 2w + dy, double 2(lane + sh) + dx + 1 -- consecutive lanes 2
+// doubles apart, conflict-free.  Each warp verifies its own row line against
+// the closed form (as the z-sweep kernel does) and otherwise sums its rows
+// from global memory; one CTA barrier per tile publishes the staged pairs.
+constexpr int kT4W = 32;
+constexpr int kT4Plane = 2 * (kT4W + 1) + 2;  // 68 doubles: 33 pairs + pad (16 B multiple)
+template <int H>
+constexpr int t4_stage_d() { return 4 * H * kT4Plane; }  // doubles per stage: 4H planes
+constexpr int kT4E = 8;  // column indices per lane (256 per warp-step)
+
+struct T4Geom {
+    int K, z0, z1, c_lo, c_hi, g;
+    int na, nb;        // tiles along x (32 rows), along y (4 row lines)
+    int ch;            // row planes per item
+    int n_items;
+};
+
+struct T4Cursor {
+    int item, ta, tb, c, c1;
+    __device__ __forceinline__ void set(const T4Geom &G, int it) {
+        item = it;
+        if (it < G.n_items) {
+            const int col = it % (G.na * G.nb), chunk = it / (G.na * G.nb);
+            ta = col % G.na;
+            tb = col / G.na;
+            c = G.c_lo + chunk * G.ch;
+            c1 = min(G.c_hi, c + G.ch);
+        }
+    }
+    __device__ __forceinline__ void next(const T4Geom &G) {
+        if (item >= G.n_items) return;
+        if (++c >= c1) set(G, item + (int)gridDim.x);
+    }
+};
+
+struct T4Tile {
+    int a0, n, b0, c;
+    bool valid;
+};
+
+template <int H>
+__device__ __forceinline__ T4Tile t4_tile(const T4Geom &G, const T4Cursor &C) {
+    T4Tile T;
+    T.valid = C.item < G.n_items;
+    T.a0 = C.ta * kT4W;
+    T.n = min(kT4W, G.g - T.a0);
+    T.b0 = C.tb * H;
+    T.c = C.c;
+    return T;
+}
+
+// cp.async the tile's element-row halves into one stage (chunks of 16 B)
+template <int H>
+__device__ __forceinline__ void t4_stage(const T4Geom &G, const T4Tile &T, const double *__restrict__ q,
+                                         double *stg) {
+    const int xlo = max(T.a0 - 1, 0);
+    const int nel = min(T.a0 + T.n - 1, G.K - 1) - xlo + 1;
+    const int zplane = G.K * G.K * 8;  // (nl < 2^31: 32-bit offsets)
+    // chunk u: plane pl = u % 4H = dz*2H + 2*ey3 + jn - 1, element e = u / 4H;
+    // node pair (i = 0, 1) at j = jn, k = 1 - dz of element (xlo + e, b0-1+ey3, c-1+dz)
+    const int base = (T.c - 1 - G.z0) * zplane + ((T.b0 - 1) * G.K + xlo) * 8;
+    const bool inner = T.b0 >= 1 && T.b0 + H - 1 <= G.K - 1 && T.c - 1 >= G.z0 && T.c <= G.z1 - 1;
+    for (int u = threadIdx.x; u < 4 * H * nel; u += H * 32) {
+        const int pl = u % (4 * H), e = u / (4 * H);
+        const int dz = pl / (2 * H), pp = pl % (2 * H) + 1, ey3 = pp >> 1, jn = pp & 1;
+        if (!inner) {
+            const int ey = T.b0 - 1 + ey3, ez = T.c - 1 + dz;
+            if (ey < 0 || ey > G.K - 1 || ez < G.z0 || ez > G.z1 - 1) continue;
+        }
+        const int off = base + dz * zplane + (ey3 * G.K + e) * 8 + (1 - dz) * 4 + jn * 2;
+        cp_async16(stg + pl * kT4Plane + 2 * e, q + off);
+    }
+}
+
+// Warp w reads exactly the four planes dz*8 + 2w + dy (its row line's runs
+// ey = b0-1+w+dy with j-half 1-dy), and no other warp reads them: so each
+// warp stages its own four planes (local plane lp = dz*2 + dy) into a
+// private ring and needs no CTA barrier -- the warps of a CTA run
+// independent pipelines.
+__device__ __forceinline__ void t4_stage_warp(const T4Geom &G, const T4Tile &T, int w, int lane,
+                                              const double *__restrict__ q, double *stg) {
+    if (T.b0 + w >= G.g) return;
+    const int xlo = max(T.a0 - 1, 0);
+    const int nel = min(T.a0 + T.n - 1, G.K - 1) - xlo + 1;
+    const int zplane = G.K * G.K * 8;
+    const int base = (T.c - 1 - G.z0) * zplane + ((T.b0 - 1) * G.K + xlo) * 8;
+    const bool inner = T.b0 + w >= 1 && T.b0 + w + 1 <= G.K - 1 && T.c - 1 >= G.z0 && T.c <= G.z1 - 1;
+    for (int u = lane; u < 4 * nel; u += 32) {
+        const int lp = u & 3, e = u >> 2;
+        const int dz = lp >> 1, dy = lp & 1;
+        const int ey3 = w + dy, jn = 1 - dy;
+        if (!inner) {
+            const int ey = T.b0 - 1 + ey3, ez = T.c - 1 + dz;
+            if (ey < 0 || ey > G.K - 1 || ez < G.z0 || ez > G.z1 - 1) continue;
+        }
+        const int off = base + dz * zplane + (ey3 * G.K + e) * 8 + (1 - dz) * 4 + jn * 2;
+        cp_async16(stg + lp * kT4Plane + 2 * e, q + off);
+    }
+}
+
+// per-warp row data of one tile: column ids (8 per lane), the lane's row
+// start, the row line's entry range (e0, end: loaded one tile earlier, so
+// the column loads do not wait on them)
+struct T4Rows {
+    int col[kT4E];
+    int lo, end, e0;
+};
+
+__device__ __forceinline__ int64_t t4_r0(const T4Geom &G, const T4Tile &T, int w) {
+    return ((int64_t)(T.c - G.c_lo) * G.g + (T.b0 + w)) * G.g + T.a0;
+}
+
+__device__ __forceinline__ void t4_load_meta(const T4Geom &G, const T4Tile &T, int w,
+                                             const int32_t *__restrict__ rs, int &e0, int &end) {
+    e0 = end = 0;
+    if (!T.valid || T.b0 + w >= G.g) return;
+    const int64_t r0 = t4_r0(G, T, w);
+    e0 = __ldg(rs + r0);
+    end = __ldg(rs + r0 + T.n);
+}
+
+__device__ __forceinline__ void t4_load_rows(const T4Geom &G, const T4Tile &T, int w, int lane, int e0, int end,
+                                             const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
+                                             T4Rows &R) {
+    R.e0 = e0;
+    R.end = end;
+    R.lo = 0;
+    if (!T.valid || T.b0 + w >= G.g) return;
+    R.lo = ld_stream(rs + t4_r0(G, T, w) + (lane < T.n ? lane : T.n));
+    const int ne = end - e0;
+#pragma unroll
+    for (int j = 0; j < kT4E; j++)
+        if (lane + 32 * j < ne) R.col[j] = ld_stream(ci + e0 + lane + 32 * j);
+}
+
+template <int H, int NB, int MINB, bool WS>
+__global__ void __launch_bounds__(H * 32, MINB)
+    k_bs6_tile4(T4Geom G, const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
+                const double *__restrict__ q, double *__restrict__ out, const double *__restrict__ carry,
+                int64_t ncarry) {
+    extern __shared__ __align__(16) double stg_all[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ystride = G.K * 8, zstride = G.K * ystride;
+    if ((int)blockIdx.x >= G.n_items) return;
+    T4Cursor C;
+    C.set(G, (int)blockIdx.x);
+    T4Tile T = t4_tile<H>(G, C);
+    C.next(G);
+    T4Tile T1 = t4_tile<H>(G, C);
+    C.next(G);  // C: two tiles ahead of T
+    // stage buffers: CTA-shared (NB x 16 planes) or warp-private (per warp NB x 4 planes)
+    double *stg = WS ? stg_all + w * (NB * 4 * kT4Plane) : stg_all;
+    constexpr int SS = WS ? 4 * kT4Plane : t4_stage_d<H>();  // doubles per stage
+    auto stage = [&](const T4Tile &X, double *dst) {
+        if (WS)
+            t4_stage_warp(G, X, w, lane, q, dst);
+        else
+            t4_stage<H>(G, X, q, dst);
+    };
+    stage(T, stg);
+    cp_async_commit();
+    if (T1.valid) stage(T1, stg + SS);
+    cp_async_commit();
+    T4Rows R;
+    int m0, m1;  // entry range of tile + 1
+    {
+        int a0_, a1_;
+        t4_load_meta(G, T, w, rs, a0_, a1_);
+        t4_load_rows(G, T, w, lane, a0_, a1_, rs, ci, R);
+    }
+    t4_load_meta(G, T1, w, rs, m0, m1);
+    int buf = 0;
+    while (T.valid) {
+        // the buffer staged below was last read NB-2 tiles ago: by this warp
+        // only (WS), or -- with 3 buffers -- by any warp of the CTA
+        if (WS)
+            __syncwarp();
+        else if (NB == 3)
+            __syncthreads();
+        const T4Tile T2 = t4_tile<H>(G, C);
+        C.next(G);
+        if (T2.valid) stage(T2, stg + ((buf + 2) % NB) * SS);
+        cp_async_commit();
+        // this warp's row line: verify against the closed form (z-sweep kernel's fast paths)
+        const int b = T.b0 + w;
+        const int nrows = b < G.g ? T.n : 0;
+        const int ne = R.end - R.e0;
+        const bool first = T.a0 == 0, last = T.a0 + T.n == G.g;
+        const int xlo = max(T.a0 - 1, 0);
+        bool ok = nrows > 0 && b >= 1 && b <= G.g - 2 && T.c - 1 >= G.z0 && T.c <= G.z1 - 1 && ne <= kT4E * 32;
+        if (ok) {
+            const int s0 = first ? 4 : 0, r1 = first ? 1 : 0;
+            const int nfull = nrows - r1 - (last ? 1 : 0);
+            ok = ne == s0 + 8 * nfull + (last ? 4 : 0);
+            if (lane < nrows) ok = ok && R.lo - R.e0 == (lane == 0 && first ? 0 : s0 + 8 * (lane - r1));
+            const int B0 = ((((T.c - 1 - G.z0) * G.K + (b - 1)) * G.K) + T.a0 - 1) * 8 + 7;
+            const int jl = (lane - s0) & 7;
+            const int X = tl_col(B0, r1 + ((lane - s0) >> 3), jl, ystride, zstride);
+            if (!first && !last) {  // (warp-uniform) 32 rows of 8: column X + 32 j
+#pragma unroll
+                for (int j = 0; j < kT4E; j++) ok = ok && (lane + 32 * j >= ne || R.col[j] == X + 32 * j);
+            } else {
+#pragma unroll
+                for (int j = 0; j < kT4E; j++) {
+                    const int k = lane + 32 * j, kp = k - s0;
+                    int want = X + 32 * j;
+                    if (kp < 0)
+                        want = tl_col(B0, 0, 2 * k + 1, ystride, zstride);
+                    else if (kp >= 8 * nfull)
+                        want = tl_col(B0, r1 + nfull, 2 * (kp - 8 * nfull), ystride, zstride);
+                    ok = ok && (k >= ne || R.col[j] == want);
+                }
+            }
+        }
+        const bool fast = __all_sync(0xffffffffu, ok);
+        int hi = __shfl_down_sync(0xffffffffu, R.lo, 1);
+        if (lane == nrows - 1) hi = R.end;
+        const int lo = R.lo;
+        // the next tile's row data (registers free after the compares), the
+        // entry range of the tile after it
+        t4_load_rows(G, T1, w, lane, m0, m1, rs, ci, R);
+        t4_load_meta(G, T2, w, rs, m0, m1);
+        cp_async_wait<2>();  // this tile's pairs (own copies) ...
+        if (WS)
+            __syncwarp();  // ... and the warp's
+        else
+            __syncthreads();  // ... and the CTA's
+        if (lane < nrows) {
+            const int64_t r = ((int64_t)(T.c - G.c_lo) * G.g + b) * G.g + T.a0 + lane;
+            double acc = r < ncarry ? carry[r] : 0.0;
+            if (fast) {
+                const double *st = stg + buf * SS + (WS ? 0 : 2 * (w * kT4Plane)) + 2 * (lane + T.a0 - 1 - xlo) + 1;
+                const bool no_dx0 = first && lane == 0, no_dx1 = last && lane == nrows - 1;
+                // entry j = dz*4 + dy*2 + dx: plane dz*8 + 2w + dy, double 2(lane+sh) + dx + 1
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const int dz = j >> 2, dy = (j >> 1) & 1, dx = j & 1;
+                    if (!(dx ? no_dx1 : no_dx0)) acc = add(acc, st[(WS ? dz * 2 + dy : dz * 2 * H + dy) * kT4Plane + dx]);
+                }
+            } else {  // any other CSR: straight from global memory
+#pragma unroll 1
+                for (int k = lo; k < hi; k++) acc = add(acc, __ldg(q + __ldg(ci + k)));
+            }
+            st_stream(out + r, acc);
+        }
+        buf = (buf + 1) % NB;
+        T = T1;
+        T1 = T2;
+    }
+}
+
 }  // namespace
 }  // namespace sb
 
@@ -294,6 +556,51 @@ int sb_bs6_gather_tiled(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_
     G.g = (int)g;
     G.na = (int)((g + kTlT - 1) / kTlT);
     const int64_t ncols = (int64_t)G.na * g, nc = c_hi - c_lo;
+    // A/B: "1" = one-row-line tiles, "3b" = 3 stage buffers / 8 CTAs per SM
+    // (4 buffers / 6 CTAs per SM by default: measured 4,776 vs 4,593 GB/s at N=1)
+    const char *kv = getenv("SB200_BS6_TILE_KERNEL");
+    if (!kv || kv[0] != '1') {
+        T4Geom H{};
+        H.K = K;
+        H.z0 = z0;
+        H.z1 = z1;
+        H.c_lo = c_lo;
+        H.c_hi = c_hi;
+        H.g = (int)g;
+        H.na = (int)((g + kT4W - 1) / kT4W);
+        // variants (A/B): 4b (default) 4 row lines, 4 CTA-shared buffers, 6 CTAs/SM;
+        // 3b: 3 buffers, 8/SM; w4 / w3: warp-private buffers; h8: 8 row lines, 3 buffers, 4/SM
+        const bool h8 = kv && kv[0] == 'h';
+        const bool four = !h8 && !(kv && (kv[0] == '3' || (kv[0] == 'w' && kv[1] == '3')));
+        const bool ws = kv && kv[0] == 'w';
+        const int rows_y = h8 ? 8 : 4;
+        H.nb = (int)((g + rows_y - 1) / rows_y);
+        using K4 = void (*)(T4Geom, const int32_t *, const int32_t *, const double *, double *, const double *,
+                            int64_t);
+        const K4 k4 = h8 ? k_bs6_tile4<8, 3, 4, false>
+                         : ws ? (four ? k_bs6_tile4<4, 4, 6, true> : k_bs6_tile4<4, 3, 8, true>)
+                              : (four ? k_bs6_tile4<4, 4, 6, false> : k_bs6_tile4<4, 3, 8, false>);
+        const size_t smem4 = (size_t)(h8 ? 3 : (four ? 4 : 3)) * 4 * rows_y * kT4Plane * sizeof(double);
+        int rc4 = cuda_check(cudaFuncSetAttribute((const void *)k4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)smem4), "sb_bs6_gather_tiled: shared memory");
+        if (rc4) return rc4;
+        int per_sm4 = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm4, (const void *)k4, rows_y * 32, smem4);
+        const int64_t gmax = (int64_t)sm_count() * std::max(1, per_sm4);
+        const int64_t ncols4 = (int64_t)H.na * H.nb, nc4 = c_hi - c_lo;
+        int64_t nch4 = std::max<int64_t>(1, std::min<int64_t>(nc4, (8 * gmax + ncols4 - 1) / ncols4));
+        H.ch = (int)((nc4 + nch4 - 1) / nch4);
+        nch4 = (nc4 + H.ch - 1) / H.ch;
+        if (ncols4 * nch4 > INT_MAX) {
+            set_error("sb_bs6_gather_tiled: too many tiles");
+            return SB_E_RANGE;
+        }
+        H.n_items = (int)(ncols4 * nch4);
+        const int64_t grid4 = std::min<int64_t>(H.n_items, gmax);
+        k4<<<(unsigned)grid4, rows_y * 32, smem4, as_stream(stream)>>>(H, row_starts, col_ids, q_local, out, carry_in,
+                                                                       n_carry);
+        return launch_check("sb_bs6_gather_tiled");
+    }
     const auto k = k_bs6_tile1<8>;
     const size_t smem = (size_t)kTlBufs * kTlStage * sizeof(double);
     int rc = cuda_check(cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
