@@ -143,36 +143,6 @@ int sb_bs6_gather_halo(const int32_t *send_plan, int64_t send_nblk, const int32_
                        const double *q, uint64_t *sync, uint64_t *peer_ready, uint64_t *peer_ack,
                        sb_stream_t stream);
 
-/* TMA-staged BS6 for structured operators of low order (p <= 2; the fast
- * path there).  A tile is ey*p x ez*p row lines (y, z) x w rows (x) of the
- * mesh.py:73-97 numbering; the producer warp of a persistent kernel copies the
- * (ey+1)(ez+1) contiguous element runs of q_local the tile reads, and its
- * col_ids / row_starts slices, into shared memory with cp.async.bulk, so the
- * per-entry gathers never go through the L1 tag path.  sb_bs6_staged_init
- * (host only) fills the tile geometry for the slab form of the operator
- * (z0/z1 elements, c_lo/c_hi row planes; whole mesh: 0, K, 0, K*p+1; ey, ez,
- * w <= 0 pick the measured defaults for p); the plan holds
- * n_tiles * words_per_tile int32 words and is filled once per operator by
- * sb_bs6_staged_make_plan.  The gather works for ANY CSR with those rows (an
- * entry whose column lies outside its tile's staged runs is read from global
- * memory): results are bitwise those of sb_bs6_gather.  All pointers 16-byte
- * aligned. */
-typedef struct {
-    int32_t K, p, z0, z1, c_lo, c_hi; /* operator geometry (slab form) */
-    int32_t ey, ez, w;                /* tile: ey x ez elements of row lines, w rows */
-    int32_t words_per_tile, max_segments, max_runs;
-    int32_t rs_cap, ci_cap, q_cap, vt_cap; /* staging capacities per tile (elements) */
-    int64_t n_tiles;
-    int64_t n_local; /* length of q_local: the slab's element-local DOFs */
-} sb_bs6_staged_t;
-int sb_bs6_staged_init(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_lo, int32_t c_hi,
-                       int32_t ey, int32_t ez, int32_t w, sb_bs6_staged_t *info);
-int sb_bs6_staged_make_plan(const sb_bs6_staged_t *info, const int32_t *row_starts, int32_t *plan,
-                            sb_stream_t stream);
-int sb_bs6_gather_staged(const sb_bs6_staged_t *info, const int32_t *plan,
-                         const int32_t *row_starts, const int32_t *col_ids, int64_t ng, int64_t nl,
-                         const double *q_local, double *out, const double *carry_in,
-                         int64_t n_carry, sb_stream_t stream);
 
 /* z-sweep BS6 for structured operators of order p <= 2 (the fast path
  * there; csrc/sb_gs_sweep.cu).  The operator's rows must be the lattice rows

@@ -36,17 +36,6 @@ _c_int, _c_i64, _c_dbl, _c_vp, _c_size = (ctypes.c_int, ctypes.c_int64, ctypes.c
                                           ctypes.c_void_p, ctypes.c_size_t)
 
 
-class Bs6Staged(ctypes.Structure):
-    """sb_bs6_staged_t (include/sb200.h): tile geometry of the TMA-staged BS6."""
-
-    _fields_ = [(n, ctypes.c_int32) for n in (
-        "K", "p", "z0", "z1", "c_lo", "c_hi", "ey", "ez", "w", "words_per_tile", "max_segments",
-        "max_runs", "rs_cap", "ci_cap", "q_cap", "vt_cap")] + [("n_tiles", ctypes.c_int64),
-                                                                ("n_local", ctypes.c_int64)]
-
-
-_c_st = ctypes.POINTER(Bs6Staged)
-
 # name -> (restype, argtypes); mirrors include/sb200.h
 _SIGS = {
     "sb_version": (_c_int, []),
@@ -97,11 +86,6 @@ _SIGS = {
     "sb_lsa_bs4_dot": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
     "sb_lsa_bs5_fused_cg_update": (_c_int, [_c_dbl, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64,
                                             _c_vp, _c_vp, _c_vp, _c_vp]),
-    "sb_bs6_staged_init": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
-                                    _c_int, _c_st]),
-    "sb_bs6_staged_make_plan": (_c_int, [_c_st, _c_vp, _c_vp, _c_vp]),
-    "sb_bs6_gather_staged": (_c_int, [_c_st, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp,
-                                      _c_i64, _c_vp]),
     "sb_bs6_gather_sweep": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_vp, _c_vp, _c_i64,
                                      _c_i64, _c_vp, _c_vp, _c_vp, _c_i64, _c_vp]),
     "sb_bs6_gather_halo": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_vp, _c_vp, _c_i64,

@@ -10,7 +10,7 @@
 // gathers into shared-memory reads (2 wavefronts per warp instruction at
 // p = 1: the four element runs a row line reads are bank-disjoint), but it
 // only pays if the staging stays close to one read of q: the r02 tile kernel
-// (sb_gs_staged.cu) re-read every element run for each 2x2 patch of row lines
+// (removed; profiles/r02_bs6_staged.md) re-read every element run for each 2x2 patch of row lines
 // (1.75x the algorithmic bytes through L2) and topped out at 2.9 TB/s.
 //
 // Here a CTA owns a column of rows -- W = 32 rows along x times H row lines

@@ -92,14 +92,6 @@ def bs6_gather_into(op, q_local: torch.Tensor, out: torch.Tensor, carry=None) ->
                                          None if carry is None else carry.data_ptr(), ncarry,
                                          _lib.stream_handle(dev)), "bs6_gather")
         return out
-    st = op.staged() if hasattr(op, "staged") and q_local.data_ptr() % 16 == 0 else None
-    if st is not None:
-        info, splan = st
-        _lib.check(L.sb_bs6_gather_staged(info, splan.data_ptr(), op.row_starts_dev.data_ptr(),
-                                          op.col_ids_dev.data_ptr(), op.ng, op.nl, q_local.data_ptr(),
-                                          out.data_ptr(), None if carry is None else carry.data_ptr(),
-                                          ncarry, _lib.stream_handle(dev)), "bs6_gather")
-        return out
     plan = op.plan() if hasattr(op, "plan") else None
     if plan is not None:
         _lib.check(L.sb_bs6_gather_planned(plan.data_ptr(), op.n_blocks, op.nodes_per_block,

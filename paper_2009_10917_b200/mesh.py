@@ -231,37 +231,6 @@ class GatherOp(_IndexArrays):
         object.__setattr__(self, "_plan", p)
         return p
 
-    def staged(self):
-        """(sb_bs6_staged_t, plan) of the TMA-staged BS6 kernel
-        (csrc/sb_gs_staged.cu), built once per operator; None unless the
-        operator is a structured one of order p <= 2.  Opt-in
-        (SB200_BS6_STAGED=1): measured slower than the super-block kernel
-        (profiles/r02_bs6_staged.md); SB200_BS6_TILE="ey,ez,w" overrides
-        the tile shape (A/B runs)."""
-        st = self.__dict__.get("_staged", False)
-        if st is not False:
-            return st
-        st = None
-        geo = self.geometry
-        if geo is not None and os.environ.get("SB200_BS6_STAGED", "0") == "1":
-            rs, ci = self.row_starts_dev, self.col_ids_dev
-            if rs.data_ptr() % 16 == 0 and ci.data_ptr() % 16 == 0:
-                tile = [int(v) for v in os.environ.get("SB200_BS6_TILE", "0,0,0").split(",")]
-                L = _lib.lib()
-                info = _lib.Bs6Staged()
-                rc = L.sb_bs6_staged_init(*geo, *tile, info)
-                if rc == _lib.SB_OK:
-                    dev = rs.device
-                    plan = torch.empty(max(1, info.n_tiles * info.words_per_tile), dtype=torch.int32,
-                                       device=dev)
-                    _lib.check(L.sb_bs6_staged_make_plan(info, rs.data_ptr(), plan.data_ptr(),
-                                                         _lib.stream_handle(dev)), "bs6 staged plan")
-                    # consumers may run on other streams: the plan is complete once built
-                    torch.cuda.current_stream(dev).synchronize()
-                    st = (info, plan)
-        object.__setattr__(self, "_staged", st)
-        return st
-
 
 def build_mesh(K: int, p: int, device=None) -> MeshConnectivity:
     """mesh.py:73-97: number the nodes of a structured K*K*K mesh of order-p hexahedra."""
