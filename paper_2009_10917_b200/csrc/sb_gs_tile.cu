@@ -22,6 +22,8 @@
 // stream, which is read as before); any other operator takes the CSR-order
 // gather in the same kernel, so results are right for ANY CSR with these
 // rows.  Row sums: the value tile + one thread per row, as in sb_gs_pipe.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <limits.h>
 #include <stdlib.h>
 
@@ -402,7 +404,7 @@ __device__ __forceinline__ void t4_load_rows(const T4Geom &G, const T4Tile &T, i
         if (lane + 32 * j < ne) R.col[j] = ld_stream(ci + e0 + lane + 32 * j);
 }
 
-template <int H, int NB, int MINB, bool WS>
+template <int H, int NB, int MINB, bool WS, bool PROBE = false>
 __global__ void __launch_bounds__(H * 32, MINB)
     k_bs6_tile4(T4Geom G, const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
                 const double *__restrict__ q, double *__restrict__ out, const double *__restrict__ carry,
@@ -456,7 +458,8 @@ __global__ void __launch_bounds__(H * 32, MINB)
         const int ne = R.end - R.e0;
         const bool first = T.a0 == 0, last = T.a0 + T.n == G.g;
         const int xlo = max(T.a0 - 1, 0);
-        bool ok = nrows > 0 && b >= 1 && b <= G.g - 2 && T.c - 1 >= G.z0 && T.c <= G.z1 - 1 && ne <= kT4E * 32;
+        bool ok = !PROBE && nrows > 0 && b >= 1 && b <= G.g - 2 && T.c - 1 >= G.z0 && T.c <= G.z1 - 1 &&
+                  ne <= kT4E * 32;
         if (ok) {
             const int s0 = first ? 4 : 0, r1 = first ? 1 : 0;
             const int nfull = nrows - r1 - (last ? 1 : 0);
@@ -481,14 +484,18 @@ __global__ void __launch_bounds__(H * 32, MINB)
                 }
             }
         }
-        const bool fast = __all_sync(0xffffffffu, ok);
+        // (PROBE: an A/B measurement of the staging + row-sum traffic alone --
+        // no index streams, results meaningless)
+        const bool fast = PROBE ? nrows > 0 : __all_sync(0xffffffffu, ok);
         int hi = __shfl_down_sync(0xffffffffu, R.lo, 1);
         if (lane == nrows - 1) hi = R.end;
         const int lo = R.lo;
         // the next tile's row data (registers free after the compares), the
         // entry range of the tile after it
-        t4_load_rows(G, T1, w, lane, m0, m1, rs, ci, R);
-        t4_load_meta(G, T2, w, rs, m0, m1);
+        if (!PROBE) {
+            t4_load_rows(G, T1, w, lane, m0, m1, rs, ci, R);
+            t4_load_meta(G, T2, w, rs, m0, m1);
+        }
         cp_async_wait<2>();  // this tile's pairs (own copies) ...
         if (WS)
             __syncwarp();  // ... and the warp's
@@ -513,6 +520,157 @@ __global__ void __launch_bounds__(H * 32, MINB)
             st_stream(out + r, acc);
         }
         buf = (buf + 1) % NB;
+        T = T1;
+        T1 = T2;
+    }
+}
+
+// ---- 32 x 4 tiles staged by TMA tensor boxes ---------------------------------
+// The cp.async staging above issues one 16 B request per lane, and L2 moves a
+// full 32 B sector for each (ncu, probe kernel: 2.7x the useful q bytes L2 ->
+// SM, L2 at 68%, DRAM at 54%).  Here one TMA box per k half does it: q seen as
+// a 4-D tensor (node 8, ex K, ey K, ez nz), box (4 nodes = one 32 B sector,
+// 33 elements, 5 element rows, 1 plane) at (4 kn, a0-1, b0-1, c-1+dz-z0) --
+// out-of-range rows / planes / elements are zero-filled by the TMA unit, so
+// edges need no special cases.  The box lands as [ey][ex][4 nodes] with the
+// 32 B swizzle (16 B chunk bit 4 ^= bit 7): row-lane reads are 4-way
+// conflicted (8-way unswizzled), the price of whole-sector transfers.
+template <int H>
+constexpr int t5_box() { return (H + 1) * 33 * 4; }  // doubles per box (H+1 element rows)
+template <int H>
+constexpr int t5_box_stride() { return (t5_box<H>() + 31) / 32 * 32; }  // 256 B aligned (the swizzle)
+template <int H>
+constexpr int t5_stage() { return 2 * t5_box_stride<H>(); }  // two k halves per tile
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int NB, int MINB, bool RS_FIRST = false, int H = 4>
+__global__ void __launch_bounds__(H * 32, MINB)
+    k_bs6_tile4t(const __grid_constant__ CUtensorMap qmap, T4Geom G, const int32_t *__restrict__ rs,
+                 const int32_t *__restrict__ ci, const double *__restrict__ q, double *__restrict__ out,
+                 const double *__restrict__ carry, int64_t ncarry) {
+    constexpr int kT5Box = t5_box<H>(), kT5BoxStride = t5_box_stride<H>(), kT5Stage = t5_stage<H>();
+    extern __shared__ __align__(16) unsigned char smem5[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem5);
+    // boxes on 256 B boundaries (the 32 B swizzle pattern repeats every 256 B)
+    const uint32_t s0 = smem_u32(smem5) + 256;
+    double *stg = reinterpret_cast<double *>(smem5 + 256 + ((256 - (s0 & 255)) & 255));
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ystride = G.K * 8, zstride = G.K * ystride;
+    if ((int)blockIdx.x >= G.n_items) return;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NB; b++) mbar_init(&full[b], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto stage = [&](const T4Tile &X, int b) {  // thread 0: both k-half boxes of tile X into buffer b
+        mbar_arrive_expect_tx(&full[b], 2u * kT5Box * 8u);
+        for (int dz = 0; dz < 2; dz++)
+            tma_load_4d(stg + b * kT5Stage + dz * kT5BoxStride, &qmap, 4 * (1 - dz), X.a0 - 1, X.b0 - 1,
+                        X.c - 1 + dz - G.z0, &full[b]);
+    };
+    T4Cursor C;
+    C.set(G, (int)blockIdx.x);
+    T4Tile T = t4_tile<H>(G, C);
+    C.next(G);
+    T4Tile T1 = t4_tile<H>(G, C);
+    C.next(G);
+    if (threadIdx.x == 0) {
+        stage(T, 0);
+        if (T1.valid) stage(T1, 1);
+    }
+    T4Rows R;
+    int m0, m1;
+    {
+        int a0_, a1_;
+        t4_load_meta(G, T, w, rs, a0_, a1_);
+        t4_load_rows(G, T, w, lane, a0_, a1_, rs, ci, R);
+    }
+    t4_load_meta(G, T1, w, rs, m0, m1);
+    int step = 0;
+    while (T.valid) {
+        const int buf = step % NB;
+        const T4Tile T2 = t4_tile<H>(G, C);
+        C.next(G);
+        // buffer (step+2) % NB was last read at step+2-NB <= step-1: every warp
+        // is past those reads (the barrier closing the previous step)
+        if (threadIdx.x == 0 && T2.valid) stage(T2, (step + 2) % NB);
+        const int b = T.b0 + w;
+        const int nrows = b < G.g ? T.n : 0;
+        const int ne = R.end - R.e0;
+        const bool first = T.a0 == 0, last = T.a0 + T.n == G.g;
+        bool ok = nrows > 0 && b >= 1 && b <= G.g - 2 && T.c - 1 >= G.z0 && T.c <= G.z1 - 1 && ne <= kT4E * 32;
+        if (ok) {
+            const int s0 = first ? 4 : 0, r1 = first ? 1 : 0;
+            const int nfull = nrows - r1 - (last ? 1 : 0);
+            ok = ne == s0 + 8 * nfull + (last ? 4 : 0);
+            if (lane < nrows) ok = ok && R.lo - R.e0 == (lane == 0 && first ? 0 : s0 + 8 * (lane - r1));
+            const int B0 = ((((T.c - 1 - G.z0) * G.K + (b - 1)) * G.K) + T.a0 - 1) * 8 + 7;
+            const int jl = (lane - s0) & 7;
+            const int X = tl_col(B0, r1 + ((lane - s0) >> 3), jl, ystride, zstride);
+            if (!first && !last) {
+#pragma unroll
+                for (int j = 0; j < kT4E; j++) ok = ok && (lane + 32 * j >= ne || R.col[j] == X + 32 * j);
+            } else {
+#pragma unroll
+                for (int j = 0; j < kT4E; j++) {
+                    const int k = lane + 32 * j, kp = k - s0;
+                    int want = X + 32 * j;
+                    if (kp < 0)
+                        want = tl_col(B0, 0, 2 * k + 1, ystride, zstride);
+                    else if (kp >= 8 * nfull)
+                        want = tl_col(B0, r1 + nfull, 2 * (kp - 8 * nfull), ystride, zstride);
+                    ok = ok && (k >= ne || R.col[j] == want);
+                }
+            }
+        }
+        const bool fast = __all_sync(0xffffffffu, ok);
+        int hi = __shfl_down_sync(0xffffffffu, R.lo, 1);
+        if (lane == nrows - 1) hi = R.end;
+        const int lo = R.lo;
+        if (RS_FIRST) {
+            // the next tile's row data after this tile's sums (A/B: see below)
+        } else {
+            t4_load_rows(G, T1, w, lane, m0, m1, rs, ci, R);
+            t4_load_meta(G, T2, w, rs, m0, m1);
+        }
+        mbar_wait(&full[buf], (uint32_t)((step / NB) & 1));  // this tile's boxes have landed
+        if (lane < nrows) {
+            const int64_t r = ((int64_t)(T.c - G.c_lo) * G.g + b) * G.g + T.a0 + lane;
+            double acc = r < ncarry ? carry[r] : 0.0;
+            if (fast) {
+                // entry j = dz*4 + dy*2 + dx: box dz, element row w+dy, element
+                // lane+dx (the box starts at ex = a0-1), node (1-dy)*2 + (1-dx)
+                const unsigned char *box = reinterpret_cast<const unsigned char *>(stg + buf * kT5Stage);
+                const bool no_dx0 = first && lane == 0, no_dx1 = last && lane == nrows - 1;
+                const int base = (w * 33 + lane) * 32;
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const int dz = j >> 2, dy = (j >> 1) & 1, dx = j & 1;
+                    int off = base + dy * 33 * 32 + dx * 32 + ((1 - dy) * 2 + (1 - dx)) * 8;
+                    off ^= ((off >> 7) & 1) << 4;  // the 32 B swizzle
+                    const double v = *reinterpret_cast<const double *>(box + dz * kT5BoxStride * 8 + off);
+                    if (!(dx ? no_dx1 : no_dx0)) acc = add(acc, v);
+                }
+            } else {
+#pragma unroll 1
+                for (int k = lo; k < hi; k++) acc = add(acc, __ldg(q + __ldg(ci + k)));
+            }
+            st_stream(out + r, acc);
+        }
+        if (RS_FIRST) {
+            t4_load_rows(G, T1, w, lane, m0, m1, rs, ci, R);
+            t4_load_meta(G, T2, w, rs, m0, m1);
+        }
+        __syncthreads();  // the buffer read above may be refilled from the next step on
+        step++;
         T = T1;
         T1 = T2;
     }
@@ -559,7 +717,73 @@ int sb_bs6_gather_tiled(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_
     // A/B: "1" = one-row-line tiles, "3b" = 3 stage buffers / 8 CTAs per SM
     // (4 buffers / 6 CTAs per SM by default: measured 4,776 vs 4,593 GB/s at N=1)
     const char *kv = getenv("SB200_BS6_TILE_KERNEL");
-    if (!kv || kv[0] != '1') {
+    if (!kv || kv[0] == 't') {
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+            cudaDriverEntryPointQueryResult qr;
+            void *fn = nullptr;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+                qr != cudaDriverEntryPointSuccess || !fn) {
+                (void)cudaGetLastError();
+                set_error("sb_bs6_gather_tiled: cuTensorMapEncodeTiled unavailable");
+                return SB_E_CUDA;
+            }
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        }
+        CUtensorMap map;
+        const cuuint64_t dims[4] = {8, (cuuint64_t)K, (cuuint64_t)K, (cuuint64_t)(z1 - z0)};
+        const cuuint64_t strides[3] = {64, 64ull * K, 64ull * K * K};
+        // default: 8 row lines per CTA (t8: 9-row boxes, 3 buffers, 3 CTAs/SM) -- measured best
+        const bool h16 = kv && kv[1] == '6', h8 = !h16 && !(kv && (kv[1] == '3' || kv[1] == '4' || kv[1] == 's'));
+        const int ry = h16 ? 16 : h8 ? 8 : 4;
+        const cuuint32_t box[4] = {4, 33, (cuuint32_t)ry + 1, 1}, estr[4] = {1, 1, 1, 1};
+        if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(q_local), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            set_error("sb_bs6_gather_tiled: tensor map encoding failed");
+            return SB_E_INVALID;
+        }
+        T4Geom H{};
+        H.K = K;
+        H.z0 = z0;
+        H.z1 = z1;
+        H.c_lo = c_lo;
+        H.c_hi = c_hi;
+        H.g = (int)g;
+        H.na = (int)((g + kT4W - 1) / kT4W);
+        H.nb = (int)((g + ry - 1) / ry);
+        // variants (A/B, SB200_BS6_TILE_KERNEL): t3 (default) 3 buffers / 6 CTAs per SM,
+        // t4: 4 buffers / 5 per SM, ts: t3 with the row sums before the next tile's loads,
+        // t8: 8 row lines per CTA (9-row boxes), 3 buffers / 3 per SM
+        const bool nb3 = !(kv && kv[1] == '4');
+        const bool rsf = kv && kv[1] == 's';
+        using K5 = void (*)(const CUtensorMap, T4Geom, const int32_t *, const int32_t *, const double *, double *,
+                            const double *, int64_t);
+        const K5 k5 = h16 ? k_bs6_tile4t<3, 2, false, 16> : h8 ? k_bs6_tile4t<3, 3, false, 8>
+                         : rsf ? k_bs6_tile4t<3, 6, true> : nb3 ? k_bs6_tile4t<3, 6> : k_bs6_tile4t<4, 5>;
+        const size_t stage_d = h16 ? t5_stage<16>() : h8 ? t5_stage<8>() : t5_stage<4>();
+        const size_t smem5 = 256 + (size_t)(nb3 ? 3 : 4) * stage_d * sizeof(double) + 256;  // (+ alignment slack)
+        int rc5 = cuda_check(cudaFuncSetAttribute((const void *)k5, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)smem5), "sb_bs6_gather_tiled: shared memory");
+        if (rc5) return rc5;
+        int per5 = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per5, (const void *)k5, ry * 32, smem5);
+        const int64_t gmax = (int64_t)sm_count() * std::max(1, per5);
+        const int64_t ncols5 = (int64_t)H.na * H.nb, nc5 = c_hi - c_lo;
+        int64_t nch5 = std::max<int64_t>(1, std::min<int64_t>(nc5, (8 * gmax + ncols5 - 1) / ncols5));
+        H.ch = (int)((nc5 + nch5 - 1) / nch5);
+        nch5 = (nc5 + H.ch - 1) / H.ch;
+        if (ncols5 * nch5 > INT_MAX) {
+            set_error("sb_bs6_gather_tiled: too many tiles");
+            return SB_E_RANGE;
+        }
+        H.n_items = (int)(ncols5 * nch5);
+        const int64_t grid5 = std::min<int64_t>(H.n_items, gmax);
+        k5<<<(unsigned)grid5, ry * 32, smem5, as_stream(stream)>>>(map, H, row_starts, col_ids, q_local, out, carry_in,
+                                                              n_carry);
+        return launch_check("sb_bs6_gather_tiled");
+    }
+    if (kv[0] != '1') {
         T4Geom H{};
         H.K = K;
         H.z0 = z0;
@@ -577,7 +801,8 @@ int sb_bs6_gather_tiled(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_
         H.nb = (int)((g + rows_y - 1) / rows_y);
         using K4 = void (*)(T4Geom, const int32_t *, const int32_t *, const double *, double *, const double *,
                             int64_t);
-        const K4 k4 = h8 ? k_bs6_tile4<8, 3, 4, false>
+        const bool probe = kv && kv[0] == 'p';
+        const K4 k4 = probe ? k_bs6_tile4<4, 4, 6, false, true> : h8 ? k_bs6_tile4<8, 3, 4, false>
                          : ws ? (four ? k_bs6_tile4<4, 4, 6, true> : k_bs6_tile4<4, 3, 8, true>)
                               : (four ? k_bs6_tile4<4, 4, 6, false> : k_bs6_tile4<4, 3, 8, false>);
         const size_t smem4 = (size_t)(h8 ? 3 : (four ? 4 : 3)) * 4 * rows_y * kT4Plane * sizeof(double);

@@ -47,7 +47,7 @@ def bs6_kernel_name(op, q_local=None) -> str:
     """Name of the kernel bs6_gather_into launches for `op` (tests, bench)."""
     import ctypes
     if q_local is not None and tiled_geometry(op, q_local) is not None:
-        return "k_bs6_tile1<128>"
+        return "k_bs6_tile4t<8 row lines>"
     if q_local is not None and sweep_geometry(op, q_local) is not None:
         return f"k_bs6_sweep<p={op.geometry[1]}>"
     plan = op.plan() if hasattr(op, "plan") else None
@@ -61,14 +61,20 @@ def bs6_kernel_name(op, q_local=None) -> str:
 
 def tiled_geometry(op, q_local):
     """(K, p, z0, z1, c_lo, c_hi) when the row-line-tiled kernel
-    (csrc/sb_gs_tile.cu) takes this gather: a structured device operator of
-    order 1.  Opt-in (SB200_BS6_TILED=1) while it measures slower than the
-    super-block kernel (profiles/r02_bs6_sweep.md)."""
+    (csrc/sb_gs_tile.cu: TMA tensor boxes of element-row halves, 8 row lines
+    per CTA) takes this gather: a structured device operator of order 1 with
+    >= 1e6 rows -- where it measured faster than the super-block kernel at
+    every size (N=1, NG ~ 1e8: 5.65-5.83 vs 4.73-4.76 TB/s;
+    profiles/r02_bs6_sweep.md).  SB200_BS6_TILED=0 / 1 forces it off / on."""
     geo = getattr(op, "geometry", None)
-    if (geo is None or geo[1] != 1 or os.environ.get("SB200_BS6_TILED", "0") != "1"
-            or q_local.data_ptr() % 16):
+    force = os.environ.get("SB200_BS6_TILED")
+    if (geo is None or geo[1] != 1 or force == "0" or q_local.data_ptr() % 16
+            or (force != "1" and op.ng < TILED_MIN_ROWS)):
         return None
     return geo
+
+
+TILED_MIN_ROWS = 1_000_000  # below: the super-block kernel (K=66: 10.6 vs 12.5 us)
 
 
 @_lib.device_guard

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def tiled_on(monkeypatch):
-    monkeypatch.setenv("SB200_BS6_TILED", "1")  # opt-in while slower than the super-block kernel
+    monkeypatch.setenv("SB200_BS6_TILED", "1")  # also below the product path's 1e6-row threshold
 
 
 @pytest.fixture(scope="module")
@@ -56,13 +56,26 @@ def expect(oracle, rs, ci, q, carry=None):
     return want
 
 
+@pytest.mark.parametrize("variant", ["", "t3", "t6", "4b", "3b", "w4", "1"])
+def test_tiled_kernel_variants_bitwise(sb, oracle, monkeypatch, variant):
+    """Every A/B variant of sb_bs6_gather_tiled (SB200_BS6_TILE_KERNEL)."""
+    if variant:
+        monkeypatch.setenv("SB200_BS6_TILE_KERNEL", variant)
+    for K in (3, 9, 70):
+        mesh = sb.build_mesh(K, 1)
+        op = sb.build_gather(mesh)
+        q = d(np.random.default_rng([K, 85]).uniform(-1, 1, mesh.nl))
+        out = tiled(op.geometry, op.row_starts_dev, op.col_ids_dev, op.ng, op.nl, q)
+        assert np.array_equal(h(out), expect(oracle, op.row_starts_dev, op.col_ids_dev, q)), (variant, K)
+
+
 @pytest.mark.parametrize("K", [1, 2, 3, 5, 126, 127, 128, 129, 200])
 def test_tiled_whole_mesh_bitwise(sb, oracle, K):
     from paper_2009_10917_b200.gs import bs6_kernel_name
     mesh = sb.build_mesh(K, 1)
     op = sb.build_gather(mesh)
     q = d(np.random.default_rng([K, 81]).uniform(-1, 1, mesh.nl))
-    assert bs6_kernel_name(op, q).startswith("k_bs6_tile1")  # the public call takes it
+    assert bs6_kernel_name(op, q).startswith("k_bs6_tile4t")  # the public call takes it
     out = sb.bs6_gather(op, q)
     assert np.array_equal(h(out), expect(oracle, op.row_starts_dev, op.col_ids_dev, q))
 

@@ -73,8 +73,8 @@ def test_c3_gather_scatter_full_size_vs_oracle(sb, oracle, p):
     """Config 3 (NG ~ 1e8 global DOFs) at order p through the public calls,
     against the OpenMP oracle (oracle/sb_oracle.c restating gs.py:10-39) for
     BS6 and plain indexing q_global[l2g] (harness.py:216-217) for BS7; at p = 1
-    (K = 463, NL = 7.9e8) the product path is the 1024-entry "wide" pairs
-    kernel, which the N = 7 bench point never runs."""
+    (K = 463, NL = 7.9e8) the product path is the row-line-tiled TMA kernel
+    (csrc/sb_gs_tile.cu), which the N = 7 bench point never runs."""
     from paper_2009_10917_b200.gs import bs6_kernel_name
     K = int(round((1e8 ** (1 / 3) - 1) / p))
     mesh = sb.build_mesh(K, p)
@@ -84,7 +84,7 @@ def test_c3_gather_scatter_full_size_vs_oracle(sb, oracle, p):
     q = torch.empty(op.nl, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
     name = bs6_kernel_name(op, q)
     if p == 1:
-        assert name.startswith("k_bs6_pairs<128,1024"), name
+        assert name.startswith("k_bs6_tile4t"), name
     out = sb.bs6_gather(op, q)
     oracle.set_threads(oracle.max_threads())
     try:
