@@ -151,9 +151,11 @@ int sb_bs6_gather_halo(const int32_t *send_plan, int64_t send_nblk, const int32_
  * so ng = (c_hi-c_lo)*(K*p+1)^2 and nl = K*K*(z1-z0)*(p+1)^3.  A persistent
  * kernel sweeps columns of 32 x 8 rows along z, staging each element plane
  * under a column in shared memory once (cp.async.bulk) and reading the
- * entries from there.  Columns outside the staged element runs are read from
- * global memory, so ANY CSR with these rows gives the right answer: results
- * are bitwise those of sb_bs6_gather.  No plan; q_local 16-byte aligned. */
+ * entries from there (p = 2: one lane per row, its column ids checked against
+ * the closed form; SB200_BS6_SWEEP_ROW2=0 selects the p = 1 value-tile
+ * consumer).  Columns outside the staged element runs are read from global
+ * memory, so ANY CSR with these rows gives the right answer: results are
+ * bitwise those of sb_bs6_gather.  No plan; q_local 16-byte aligned. */
 int sb_bs6_gather_sweep(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_lo, int32_t c_hi,
                         const int32_t *row_starts, const int32_t *col_ids, int64_t ng, int64_t nl,
                         const double *q_local, double *out, const double *carry_in, int64_t n_carry,

@@ -33,6 +33,11 @@
 // global memory, so the result is right for ANY CSR with these rows -- the
 // geometry only decides the speed.  A warp-step with more than 256 entries
 // sums its rows straight from global memory.
+//
+// p = 2 (k_bs6_sweep2, the default there): rows have 1-8 entries, so the
+// value tile costs more than it saves; each lane loads its own row's column
+// ids, checks them against the closed form and sums straight from the staged
+// runs (sw_step2).  SB200_BS6_SWEEP_ROW2=0 selects the p = 1 consumer.
 #include <limits.h>
 #include <stdlib.h>
 
@@ -426,6 +431,76 @@ __device__ __forceinline__ bool sw_step(const SwGeom &G, SwState<P, H> &S, SwCur
     return true;
 }
 
+// The producer warp: lane y < ny copies run y of each element plane of the
+// CTA's items into the ring (cp.async.bulk, one transaction count per plane);
+// the item geometry is computed once per item, a plane is an address increment.
+template <int P, int H>
+__device__ __forceinline__ void sw_produce(const SwGeom &G, const double *__restrict__ q, double *ring,
+                                           uint64_t *full, uint64_t *empty, int lane) {
+    const int nslot = G.nslot;
+    const int64_t grid = gridDim.x;
+    constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
+    const int64_t pstride = (int64_t)G.K * G.K * N3;  // one element plane of q_local
+    const int64_t qlim = G.nl & ~int64_t(1);          // bulk copies move whole 16 B units
+    int64_t pit = blockIdx.x;                           // L2 prefetch cursor
+    SwItem PI{};
+    int pj = 0, pseq = 0;
+    bool pok = false;
+    auto p_load = [&]() {
+        for (; pit < G.n_items; pit += grid) {
+            PI = sw_item<P, H>(G, pit);
+            if (PI.np > 0) {
+                pok = true;
+                return;
+            }
+        }
+        pok = false;
+    };
+    if (G.pfd > 0) p_load();
+    int seq = 0, slot = 0;
+    uint32_t eph = 0;
+    for (int64_t it = blockIdx.x; it < G.n_items; it += grid) {
+        const SwItem I = sw_item<P, H>(G, it);
+        const int64_t len = (int64_t)I.nx * N3;
+        int64_t cb = lane < I.ny ? sw_col<P>(G, I.xlo, I.ylo + lane, I.zf) : 0;
+        for (int j = 0; j < I.np; j++, seq++, cb += pstride) {
+            while (pok && pseq <= seq + G.pfd) {
+                if (pseq > seq && lane < PI.ny) {
+                    const int64_t pc = sw_col<P>(G, PI.xlo, PI.ylo + lane, PI.zf + pj);
+                    const int64_t pa = pc & ~int64_t(1), pe = min((pc + (int64_t)PI.nx * N3 + 1) & ~int64_t(1), qlim);
+                    if (pe > pa) bulk_prefetch_l2(q + pa, (uint32_t)(pe - pa) * 8u);
+                }
+                pseq++;
+                if (++pj >= PI.np) {
+                    pj = 0;
+                    pit += grid;
+                    p_load();
+                }
+            }
+            if (seq >= nslot) mbar_wait(&empty[slot], eph);
+            double *dst = ring + (size_t)slot * G.plane_d + (size_t)lane * G.rs_d;
+            const int64_t qa = cb & ~int64_t(1), qe = (cb + len + 1) & ~int64_t(1);
+            const int64_t ce = qe < qlim ? qe : qlim;
+            uint32_t bytes = 0;
+            if (lane < I.ny) {
+                // the odd tail past the last 16 B unit of q_local: plain
+                // stores, ordered before lane 0's arrive by the warp sync
+                if (qe > qlim)
+                    for (int64_t x = qlim > qa ? qlim : qa; x < cb + len; x++) dst[x - qa] = __ldg(q + x);
+                if (ce > qa) bytes = (uint32_t)(ce - qa) * 8u;
+            }
+            const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
+            if (lane == 0) mbar_arrive_expect_tx(&full[slot], total);
+            __syncwarp();
+            if (bytes) bulk_g2s_plain(dst, q + qa, bytes, &full[slot]);
+            if (++slot == nslot) {
+                slot = 0;
+                if (seq >= nslot) eph ^= 1u;
+            }
+        }
+    }
+}
+
 template <int P, int H, bool SWZ, int MB>
 __global__ void __launch_bounds__((H + 1) * 32, MB)
     k_bs6_sweep(SwGeom G, const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
@@ -446,72 +521,8 @@ __global__ void __launch_bounds__((H + 1) * 32, MB)
         fence_mbar_init();
     }
     __syncthreads();
-    const int64_t grid = gridDim.x;
-
     if (warp == H) {
-        // ------------------------------------------------ producer warp
-        // lane y < ny copies run y of each element plane; the item geometry
-        // is computed once per item, a plane is an address increment
-        constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
-        const int64_t pstride = (int64_t)G.K * G.K * N3;  // one element plane of q_local
-        const int64_t qlim = G.nl & ~int64_t(1);          // bulk copies move whole 16 B units
-        int64_t pit = blockIdx.x;                           // L2 prefetch cursor
-        SwItem PI{};
-        int pj = 0, pseq = 0;
-        bool pok = false;
-        auto p_load = [&]() {
-            for (; pit < G.n_items; pit += grid) {
-                PI = sw_item<P, H>(G, pit);
-                if (PI.np > 0) {
-                    pok = true;
-                    return;
-                }
-            }
-            pok = false;
-        };
-        if (G.pfd > 0) p_load();
-        int seq = 0, slot = 0;
-        uint32_t eph = 0;
-        for (int64_t it = blockIdx.x; it < G.n_items; it += grid) {
-            const SwItem I = sw_item<P, H>(G, it);
-            const int64_t len = (int64_t)I.nx * N3;
-            int64_t cb = lane < I.ny ? sw_col<P>(G, I.xlo, I.ylo + lane, I.zf) : 0;
-            for (int j = 0; j < I.np; j++, seq++, cb += pstride) {
-                while (pok && pseq <= seq + G.pfd) {
-                    if (pseq > seq && lane < PI.ny) {
-                        const int64_t pc = sw_col<P>(G, PI.xlo, PI.ylo + lane, PI.zf + pj);
-                        const int64_t pa = pc & ~int64_t(1), pe = min((pc + (int64_t)PI.nx * N3 + 1) & ~int64_t(1), qlim);
-                        if (pe > pa) bulk_prefetch_l2(q + pa, (uint32_t)(pe - pa) * 8u);
-                    }
-                    pseq++;
-                    if (++pj >= PI.np) {
-                        pj = 0;
-                        pit += grid;
-                        p_load();
-                    }
-                }
-                if (seq >= nslot) mbar_wait(&empty[slot], eph);
-                double *dst = ring + (size_t)slot * G.plane_d + (size_t)lane * G.rs_d;
-                const int64_t qa = cb & ~int64_t(1), qe = (cb + len + 1) & ~int64_t(1);
-                const int64_t ce = qe < qlim ? qe : qlim;
-                uint32_t bytes = 0;
-                if (lane < I.ny) {
-                    // the odd tail past the last 16 B unit of q_local: plain
-                    // stores, ordered before lane 0's arrive by the warp sync
-                    if (qe > qlim)
-                        for (int64_t x = qlim > qa ? qlim : qa; x < cb + len; x++) dst[x - qa] = __ldg(q + x);
-                    if (ce > qa) bytes = (uint32_t)(ce - qa) * 8u;
-                }
-                const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
-                if (lane == 0) mbar_arrive_expect_tx(&full[slot], total);
-                __syncwarp();
-                if (bytes) bulk_g2s_plain(dst, q + qa, bytes, &full[slot]);
-                if (++slot == nslot) {
-                    slot = 0;
-                    if (seq >= nslot) eph ^= 1u;
-                }
-            }
-        }
+        sw_produce<P, H>(G, q, ring, full, empty, lane);
         return;
     }
 
@@ -545,12 +556,197 @@ __global__ void __launch_bounds__((H + 1) * 32, MB)
     }
 }
 
+// ---------------------------------------------------------------- p = 2
+// Row-lane consumer for p = 2 (k_bs6_sweep2).  A p = 2 row has 1, 2, 4 or 8
+// entries (3.4 on average), so the value tile of the p = 1 path costs more
+// than it saves; instead lane = row throughout: each lane loads its own <= 8
+// column ids (one step ahead, from the row starts in the cp.async ring),
+// checks them against the closed form of its row (mesh.py:113-134 order:
+// candidates (ez, ey, ex) lexicographic, x fastest, node (kn, jn, in) =
+// lattice - 2 * element), and -- when the whole warp matches -- sums its row
+// straight from the staged element runs in ascending column order.  A run is
+// 27 doubles per element (odd), so the 32 lanes' reads of 16 + 1 elements
+// fall in distinct bank pairs: 2 wavefronts per read, the minimum for 8 B.
+// Any mismatch (a CSR that is not the closed form, rows longer than 8) sums
+// the warp's rows from global memory in the same order.
+
+__device__ __forceinline__ void sw_load_cols_row(const int *slot, const int32_t *__restrict__ ci, int lane,
+                                                 int (&col)[8]) {
+    const int lo = slot[lane], n = slot[lane + 1] - lo;
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+        if (t < n) col[t] = __ldg(ci + lo + t);
+}
+
+template <int H>
+__device__ __forceinline__ bool sw_step2(const SwGeom &G, SwState<2, H> &S, SwCursor<2, H> &ahead, int warp,
+                                         int lane, int (&colA)[8], int (&colB)[8], int *rsr,
+                                         const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
+                                         const double *__restrict__ q, double *__restrict__ out,
+                                         const double *__restrict__ carry, int64_t ncarry, uint64_t *full,
+                                         uint64_t *empty, const double *ring) {
+    constexpr int P = 2, N3 = 27;
+    const int st = S.step;
+    sw_issue_rs(ahead.rows(G), rs, lane, rsr + ((st + 4) & (kSwRsSlots - 1)) * kSwRsStride);  // step + 4
+    ahead.next(G, warp);
+    cp_async_wait<2>();
+    __syncwarp();
+    sw_load_cols_row(rsr + ((st + 1) & (kSwRsSlots - 1)) * kSwRsStride, ci, lane, colB);  // step + 1
+    sw_prefetch_cols(rsr + ((st + 2) & (kSwRsSlots - 1)) * kSwRsStride, ci, lane);       // step + 2
+    const int *cur = rsr + (st & (kSwRsSlots - 1)) * kSwRsStride;
+    const int lo0 = cur[lane], n0 = cur[lane + 1] - lo0;
+    S.step = st + 1;
+
+    const SwItem &I = S.I;
+    const int c = S.c;
+    const int nslot = G.nslot;
+    const int zlo = max(el_lo<P>(c, G.K), G.z0), zhi = min(el_hi<P>(c, G.K), G.z1 - 1);
+    if (zhi >= zlo) {
+        const int need = S.base + (zhi - I.zf) + 1;
+        for (; S.waited < need; S.waited++) {
+            mbar_wait(&full[S.wslot], S.wph);
+            if (++S.wslot == nslot) {
+                S.wslot = 0;
+                S.wph ^= 1u;
+            }
+        }
+    }
+    const int bb = I.b0 + warp;
+    if (bb < G.g) {
+        const int nrows = I.a1 - I.a0;
+        const int64_t r = ((int64_t)(c - G.c_lo) * G.g + bb) * G.g + I.a0 + lane;
+        double acc = 0.0;
+        if (lane < nrows && r < ncarry) acc = carry[r];
+        // candidates: z, y per warp (groups g = (iz, iy), m of them), x per
+        // lane (one or two); entry t of the row is group t / nx, x t % nx
+        const int ylo = el_lo<P>(bb, G.K), yhi = el_hi<P>(bb, G.K);
+        const int a = I.a0 + lane;
+        const int xlo = el_lo<P>(a, G.K), xhi = el_hi<P>(a, G.K);
+        const bool z2 = zhi > zlo, y2 = yhi > ylo, x2 = xhi > xlo;
+        const int m = zhi < zlo ? 0 : (z2 ? 2 : 1) * (y2 ? 2 : 1);
+        const int ystride = G.K * N3, zstride = G.K * ystride;
+        // column of (g, x) = Y[g] + X{0,1}; staged index = column + D[g]
+        const int cb0 = ((zlo - G.z0) * G.K + ylo) * ystride + I.xlo * N3;
+        const int y00 = cb0 + (c - 2 * zlo) * 9 + (bb - 2 * ylo) * 3;
+        const int dz = zstride - 18, dy = ystride - 6;
+        const int X0 = (xlo - I.xlo) * N3 + (a - 2 * xlo), X1 = (xhi - I.xlo) * N3 + (a - 2 * xhi);
+        int Y[4];
+        Y[0] = y00;
+        Y[1] = y00 + (y2 ? dy : dz);
+        Y[2] = y00 + dz;
+        Y[3] = y00 + dz + dy;
+        bool ok = lane >= nrows || n0 == (x2 ? 2 * m : m);
+#pragma unroll
+        for (int g = 0; g < 4; g++) {
+            const bool e0 = x2 ? colA[2 * g] == Y[g] + X0 : colA[g] == Y[g] + X0;
+            const bool e1 = !x2 || colA[2 * g + 1] == Y[g] + X1;
+            ok = ok && (g >= m || lane >= nrows || (e0 && e1));
+        }
+        if (m > 0 && __all_sync(0xffffffffu, ok)) {
+            // staged byte address of group g's run: ring slot of its z plane,
+            // run of its y, the run's 16 B-alignment shift, minus its first column
+            int sl1 = S.rslot + 1;
+            if (sl1 == nslot) sl1 = 0;
+            const uint32_t rb = smem_u32(ring);
+            const int s0 = S.rslot * G.plane_d + (ylo - I.ylo) * G.rs_d, s2 = sl1 * G.plane_d + (ylo - I.ylo) * G.rs_d;
+            const int cy = cb0 + ystride, cz = cb0 + zstride, czy = cz + ystride;
+            uint32_t E[4];
+            E[0] = rb + 8u * (uint32_t)(s0 + (cb0 & 1) - cb0 + Y[0]);
+            E[1] = y2 ? rb + 8u * (uint32_t)(s0 + G.rs_d + (cy & 1) - cy + Y[1])
+                      : rb + 8u * (uint32_t)(s2 + (cz & 1) - cz + Y[1]);
+            E[2] = rb + 8u * (uint32_t)(s2 + (cz & 1) - cz + Y[2]);
+            E[3] = rb + 8u * (uint32_t)(s2 + G.rs_d + (czy & 1) - czy + Y[3]);
+            const uint32_t x0 = 8u * (uint32_t)X0, x1 = 8u * (uint32_t)X1;
+            if (lane < nrows) {
+#pragma unroll
+                for (int g = 0; g < 4; g++) {
+                    if (g < m) {
+                        acc = add(acc, lds_f64(E[g] + x0));
+                        if (x2) acc = add(acc, lds_f64(E[g] + x1));
+                    }
+                }
+                st_stream(out + r, acc);
+            }
+        } else if (lane < nrows) {  // not the closed form: from global memory
+#pragma unroll 1
+            for (int t = lo0; t < lo0 + n0; t++) acc = add(acc, __ldg(q + __ldg(ci + t)));
+            st_stream(out + r, acc);
+        }
+    }
+
+    const int keep = (c + 1 < I.c1) ? S.base + min(max(el_lo<P>(c + 1, G.K), G.z0) - I.zf, I.np)
+                                    : S.base + I.np;
+    if (keep > S.released) {
+        __syncwarp();
+        for (; S.released < keep; S.released++) {
+            if (lane == 0) mbar_arrive(&empty[S.rslot]);
+            if (++S.rslot == nslot) S.rslot = 0;
+        }
+    }
+    if (++S.c >= I.c1) {
+        S.base += I.np;
+        S.it += gridDim.x;
+        if (S.it >= G.n_items) return false;
+        S.I = sw_item<P, H>(G, S.it);
+        S.c = S.I.c0;
+    }
+    return true;
+}
+
+template <int H, int MB>
+__global__ void __launch_bounds__((H + 1) * 32, MB)
+    k_bs6_sweep2(SwGeom G, const int32_t *__restrict__ rs, const int32_t *__restrict__ ci,
+                 const double *__restrict__ q, double *__restrict__ out, const double *__restrict__ carry,
+                 int64_t ncarry) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *empty = full + kSwMaxSlots;
+    double *ring = reinterpret_cast<double *>(smem + kSwHdr);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nslot = G.nslot;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nslot; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], H);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == H) {
+        sw_produce<2, H>(G, q, ring, full, empty, lane);
+        return;
+    }
+    if ((int64_t)blockIdx.x >= G.n_items) return;
+    SwState<2, H> S;
+    S.it = blockIdx.x;
+    S.I = sw_item<2, H>(G, S.it);
+    S.c = S.I.c0;
+    S.base = S.waited = S.wslot = S.released = S.rslot = 0;
+    S.wph = 0;
+    S.step = 0;
+    int *rsr = reinterpret_cast<int *>(ring + (size_t)nslot * G.plane_d) + warp * kSwRsSlots * kSwRsStride;
+    SwCursor<2, H> ahead;
+    ahead.set(G, S.it, warp);
+    for (int k = 0; k < 4; k++) {
+        sw_issue_rs(ahead.rows(G), rs, lane, rsr + k * kSwRsStride);
+        ahead.next(G, warp);
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    int col0[8], col1[8];
+    sw_load_cols_row(rsr, ci, lane, col0);
+    sw_prefetch_cols(rsr + kSwRsStride, ci, lane);
+    while (sw_step2<H>(G, S, ahead, warp, lane, col0, col1, rsr, rs, ci, q, out, carry, ncarry, full, empty, ring) &&
+           sw_step2<H>(G, S, ahead, warp, lane, col1, col0, rsr, rs, ci, q, out, carry, ncarry, full, empty, ring)) {
+    }
+}
+
 // tuning knobs (sb_bs6_sweep_tune; A/B runs and tests): <= 0 / < 0 = default
 int g_sw_slots = 0, g_sw_pfd = -1, g_sw_waves = 0, g_sw_swz = -1, g_sw_h = 0;
 
 template <int P, int H, int MB>
 int sweep_launch(const SwGeom &G0, const int32_t *rs, const int32_t *ci, const double *q, double *out,
-                 const double *carry, int64_t ncarry, bool swz, cudaStream_t st) {
+                 const double *carry, int64_t ncarry, bool swz, bool row2, cudaStream_t st) {
     SwGeom G = G0;
     G.nb = (G.g + H - 1) / H;
     constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
@@ -558,13 +754,16 @@ int sweep_launch(const SwGeom &G0, const int32_t *rs, const int32_t *ci, const d
     G.rs_d = (nx_max * N3 + 2 + 15) / 16 * 16;  // + the odd-start shift and 16 B rounding
     G.plane_d = ny_max * G.rs_d;
     auto smem_for = [&](int ns) {
-        return kSwHdr + (size_t)ns * G.plane_d * 8 + (size_t)H * kSwVt * 8 + (size_t)H * kSwRsSlots * kSwRsStride * 4;
+        return kSwHdr + (size_t)ns * G.plane_d * 8 + (row2 ? 0 : (size_t)H * kSwVt * 8) +
+               (size_t)H * kSwRsSlots * kSwRsStride * 4;
     };
     while (G.nslot > 3 && smem_for(G.nslot) > 227 * 1024) G.nslot--;  // large columns: a shallower ring
     const size_t smem = smem_for(G.nslot);
     using KernT = void (*)(SwGeom, const int32_t *, const int32_t *, const double *, double *, const double *,
                            int64_t);
-    const KernT k = swz ? k_bs6_sweep<P, H, true, MB> : k_bs6_sweep<P, H, false, MB>;
+    KernT k = swz ? k_bs6_sweep<P, H, true, MB> : k_bs6_sweep<P, H, false, MB>;
+    if constexpr (P == 2)
+        if (row2) k = k_bs6_sweep2<H, MB>;
     int rc = cuda_check(cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                         "sb_bs6_gather_sweep: shared memory");
     if (rc) return rc;
@@ -626,13 +825,16 @@ int sb_bs6_gather_sweep(int32_t K, int32_t p, int32_t z0, int32_t z1, int32_t c_
     G.nslot = g_sw_slots > 0 ? g_sw_slots : 4;
     G.pfd = g_sw_pfd >= 0 ? g_sw_pfd : 0;  // L2 prefetch measured slower (profiles/r02_bs6_sweep.md)
     const bool swz = g_sw_swz >= 0 ? g_sw_swz == 1 : p == 1;
+    // p = 2: the row-lane consumer (k_bs6_sweep2) unless SB200_BS6_SWEEP_ROW2=0
+    const char *r2env = getenv("SB200_BS6_SWEEP_ROW2");
+    const bool row2 = p == 2 && !(r2env && r2env[0] == '0');
     const cudaStream_t st = as_stream(stream);
     // row lines per column (one consumer warp each) and CTAs per SM: 8 / 2 by
     // default; 7 / 3 and 16 / 1 for A/B runs
     const int h = g_sw_h > 0 ? g_sw_h : 8;
-#define SB_SW(P_) (h == 7 ? sweep_launch<P_, 7, 3>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, st) \
-                  : h == 16 ? sweep_launch<P_, 16, 1>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, st) \
-                            : sweep_launch<P_, 8, 2>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, st))
+#define SB_SW(P_) (h == 7 ? sweep_launch<P_, 7, 3>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, row2, st) \
+                  : h == 16 ? sweep_launch<P_, 16, 1>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, row2, st) \
+                            : sweep_launch<P_, 8, 2>(G, row_starts, col_ids, q_local, out, carry_in, n_carry, swz, row2, st))
     const int rc = p == 1 ? SB_SW(1) : SB_SW(2);
 #undef SB_SW
     return rc;

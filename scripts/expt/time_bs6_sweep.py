@@ -53,7 +53,7 @@ def main():
                                     op.col_ids_dev.data_ptr(), op.ng, op.nl, q.data_ptr(), ref.data_ptr(), None, 0, st)
         ms = timed(planned)
         print(f"N={p:2d} K={K} planned                 {ms:.3f} ms {nb / ms / 1e6:7.0f} GB/s", flush=True)
-        for cfg in (cfgs.split(";") if p <= 2 else []):
+        for cfg in ([c for c in cfgs.split(";") if c] if p <= 2 else []):
             slots, pfd, waves, swz, h = (int(v) for v in (cfg + ",0").split(",")[:5])
             _lib.check(L.sb_bs6_sweep_tune(slots, pfd, waves, swz, h), "tune")
 

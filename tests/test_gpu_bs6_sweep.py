@@ -79,6 +79,18 @@ def test_sweep_whole_mesh_bitwise(sb, oracle, K, p):
     assert np.array_equal(h(out), expect(oracle, op.row_starts_dev, op.col_ids_dev, q))
 
 
+@pytest.mark.parametrize("K", [1, 2, 5, 11, 16, 31])
+def test_sweep_p2_value_tile_consumer(sb, oracle, monkeypatch, K):
+    """p = 2 through the p = 1 (value-tile) consumer instead of the default
+    row-lane one (SB200_BS6_SWEEP_ROW2=0): same bits."""
+    monkeypatch.setenv("SB200_BS6_SWEEP_ROW2", "0")
+    mesh = sb.build_mesh(K, 2)
+    op = sb.build_gather(mesh)
+    q = d(np.random.default_rng([K, 77]).uniform(-1, 1, mesh.nl))
+    out = sweep(op.geometry, op.row_starts_dev, op.col_ids_dev, op.ng, op.nl, q)
+    assert np.array_equal(h(out), expect(oracle, op.row_starts_dev, op.col_ids_dev, q))
+
+
 @pytest.mark.parametrize("slots,pfd,waves,swz,rows", [(3, 0, 1, -1, 0), (3, 4, 64, 0, 7), (5, 1, 2, 1, 16),
                                                    (8, 16, 8, -1, 8), (4, 0, 1000, 1, 7), (3, 2, 3, -1, 16)])
 @pytest.mark.parametrize("K,p", [(13, 1), (11, 2), (34, 1)])
