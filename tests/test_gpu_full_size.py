@@ -69,7 +69,7 @@ def test_c5_mesh_gather_scatter_whole_on_one_gpu(sb):
 
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 10, 15])
-def test_c3_gather_scatter_full_size_vs_oracle(sb, oracle, p):
+def test_c3_gather_scatter_full_size_vs_oracle(sb, oracle, monkeypatch, p):
     """Config 3 (NG ~ 1e8 global DOFs) at order p through the public calls,
     against the OpenMP oracle (oracle/sb_oracle.c restating gs.py:10-39) for
     BS6 and plain indexing q_global[l2g] (harness.py:216-217) for BS7; at p = 1
@@ -92,6 +92,12 @@ def test_c3_gather_scatter_full_size_vs_oracle(sb, oracle, p):
     finally:
         oracle.set_threads(1)
     assert np.array_equal(out.cpu().numpy(), want), name
+    if p == 1:  # the super-block kernel it replaced (wide 1024-entry pairs at this size) still serves
+        monkeypatch.setenv("SB200_BS6_TILED", "0")  # unstructured / unaligned p = 1 operators
+        name = bs6_kernel_name(op, q)
+        assert name.startswith("k_bs6_pairs<128,1024"), name
+        assert np.array_equal(sb.bs6_gather(op, q).cpu().numpy(), want), name
+        monkeypatch.delenv("SB200_BS6_TILED")
     del out, want
     ids = sb.build_scatter_ids(mesh)
     qg = torch.empty(mesh.ng, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
