@@ -193,6 +193,18 @@ int sb_bs7_scatter(const int32_t *ids, int64_t nl, const double *q_global, int64
 int sb_bs7_scatter_split(const int32_t *ids, int64_t nl, const double *q_own, int64_t n_own,
                          const double *q_halo, int64_t n_halo, double *q_local, int has_mask,
                          sb_stream_t stream);
+/* The same with two alternating halo buffers: q_halo0 or q_halo1 by the parity
+ * of (*call_count - 1), a device-side call counter that
+ * sb_lsa_barrier_advance advanced just before (so captured CUDA graphs
+ * alternate correctly on replay).  sb_bs7_halo_put copies n doubles of src
+ * into dst0 or dst1 by the parity of *call_count (before the barrier): the
+ * rank above's bottom plane into this rank's halo buffer (dist.py). */
+int sb_bs7_scatter_split_pair(const int32_t *ids, int64_t nl, const double *q_own, int64_t n_own,
+                              const double *q_halo0, const double *q_halo1, int64_t n_halo,
+                              const unsigned long long *call_count, double *q_local, int has_mask,
+                              sb_stream_t stream);
+int sb_bs7_halo_put(const double *src, double *dst0, double *dst1, int64_t n,
+                    const unsigned long long *call_count, sb_stream_t stream);
 
 /* ---- operator construction (mesh.py:73-153) ------------------------------
  * Slab form: elements with ez in [z0, z1) of the K^3 order-p mesh; the
@@ -330,6 +342,8 @@ int sb_lsa_abort(sb_lsa_t *ctx);
 int sb_lsa_halo_window(sb_lsa_t *ctx, size_t bytes);
 int sb_lsa_halo_pointers(sb_lsa_t *ctx, size_t offset, int peer, void **local, void **remote);
 int sb_lsa_barrier(sb_lsa_t *ctx, sb_stream_t stream);
+/* The barrier, then *call_count += 1 (one thread; the BS7 halo parity). */
+int sb_lsa_barrier_advance(sb_lsa_t *ctx, unsigned long long *call_count, sb_stream_t stream);
 /* Multi-GPU device-resident CG: sb_cg_pap / sb_cg_update whose reductions
  * (pAp, r.r) combine over the ranks in the same launch, so every rank's
  * sb_cg_state holds the global scalars and the ranks gate identically;

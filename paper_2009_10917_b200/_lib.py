@@ -53,6 +53,9 @@ _SIGS = {
                                _c_vp, _c_i64, _c_vp]),
     "sb_bs7_scatter": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_int, _c_vp]),
     "sb_bs7_scatter_split": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_int, _c_vp]),
+    "sb_bs7_scatter_split_pair": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i64, _c_vp, _c_vp, _c_i64, _c_vp, _c_vp,
+                                           _c_int, _c_vp]),
+    "sb_bs7_halo_put": (_c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_vp, _c_vp]),
     "sb_build_l2g": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp]),
     "sb_build_gather_csr": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp,
                                      _c_vp, _c_vp]),
@@ -79,6 +82,7 @@ _SIGS = {
     "sb_lsa_halo_window": (_c_int, [_c_vp, _c_size]),
     "sb_lsa_halo_pointers": (_c_int, [_c_vp, _c_size, _c_int, _c_vp, _c_vp]),
     "sb_lsa_barrier": (_c_int, [_c_vp, _c_vp]),
+    "sb_lsa_barrier_advance": (_c_int, [_c_vp, _c_vp, _c_vp]),
     "sb_lsa_cg_pap": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
     "sb_lsa_cg_update": (_c_int, [_c_int, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp,
                                   _c_vp, _c_vp]),

@@ -90,7 +90,10 @@ __global__ void __launch_bounds__(256) k_bs6_rows(const int32_t *__restrict__ rs
 int bs7_lanes_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,
                      cudaStream_t st);  // sb_gs_pipe.cu
 int bs7_split_launch(const int32_t *ids, int64_t nl, const double *qg, int32_t split, const double *qh,
-                     double *ql, int has_mask, cudaStream_t st);  // sb_gs_pipe.cu
+                     const double *qh1, const unsigned long long *cnt, double *ql, int has_mask,
+                     cudaStream_t st);  // sb_gs_pipe.cu
+int halo_put_launch(const double *src, double *dst0, double *dst1, int64_t n, const unsigned long long *cnt,
+                    cudaStream_t st);  // sb_gs_pipe.cu
 
 // rows straight from global memory for every operator (A/B reference point)
 int bs6_rows_launch(const int32_t *rs, const int32_t *ci, int64_t ng, const double *q, double *out,
@@ -150,7 +153,32 @@ int sb_bs7_scatter_split(const int32_t *ids, int64_t nl, const double *q_own, in
         return SB_E_INVALID;
     }
     if (nl == 0) return SB_OK;
-    return bs7_split_launch(ids, nl, q_own, (int32_t)n_own, q_halo, ql, has_mask, as_stream(s));
+    return bs7_split_launch(ids, nl, q_own, (int32_t)n_own, q_halo, nullptr, nullptr, ql, has_mask, as_stream(s));
+}
+
+int sb_bs7_scatter_split_pair(const int32_t *ids, int64_t nl, const double *q_own, int64_t n_own,
+                              const double *q_halo0, const double *q_halo1, int64_t n_halo,
+                              const unsigned long long *call_count, double *ql, int has_mask, sb_stream_t s) {
+    clear_error();
+    if (nl < 0 || n_own < 0 || n_halo < 0 || n_own > 0x7fffffffLL || !call_count ||
+        (nl > 0 && (!ids || !ql || (n_own > 0 && !q_own) || (n_halo > 0 && (!q_halo0 || !q_halo1))))) {
+        set_error("sb_bs7_scatter_split_pair: invalid arguments");
+        return SB_E_INVALID;
+    }
+    if (nl == 0) return SB_OK;
+    return bs7_split_launch(ids, nl, q_own, (int32_t)n_own, q_halo0, q_halo1, call_count, ql, has_mask,
+                            as_stream(s));
+}
+
+int sb_bs7_halo_put(const double *src, double *dst0, double *dst1, int64_t n, const unsigned long long *call_count,
+                    sb_stream_t s) {
+    clear_error();
+    if (n < 0 || (n > 0 && (!src || !dst0 || !dst1 || !call_count))) {
+        set_error("sb_bs7_halo_put: invalid arguments");
+        return SB_E_INVALID;
+    }
+    if (n == 0) return SB_OK;
+    return halo_put_launch(src, dst0, dst1, n, call_count, as_stream(s));
 }
 
 }  // extern "C"

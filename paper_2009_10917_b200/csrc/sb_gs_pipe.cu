@@ -47,11 +47,17 @@ constexpr int kBs6MinCtas = 12;
 // 128 entries and pays more L1 tag lookups per instruction.
 // SPLIT: q_global lives in two pieces -- ids < split index `qg`, ids >= split
 // index `qh` (the multi-GPU slab's own rows and the halo plane written over
-// NVLink by the rank above, dist.py DistScatter.enable_lsa).
+// NVLink by the rank above, dist.py DistScatter.enable_lsa).  With `cnt` the
+// halo is one of two alternating buffers, qh or qh1 by the call count the
+// LSA barrier advanced just before (buffer (cnt - 1) & 1): the parity lives in
+// device memory, so CUDA-graph replays alternate correctly.
 template <int T, int U, bool MASK, bool SPLIT = false>
 __global__ void __launch_bounds__(T) k_bs7_lanes(const int32_t *__restrict__ ids, int64_t nl,
                                                 const double *__restrict__ qg, double *__restrict__ ql,
-                                                int32_t split = 0, const double *__restrict__ qh = nullptr) {
+                                                int32_t split = 0, const double *__restrict__ qh = nullptr,
+                                                const double *__restrict__ qh1 = nullptr,
+                                                const unsigned long long *__restrict__ cnt = nullptr) {
+    if (SPLIT && cnt && ((*cnt - 1) & 1)) qh = qh1;
     const uint64_t pol = policy_evict_last();
     const int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x;
     int32_t d[U];
@@ -69,14 +75,30 @@ __global__ void __launch_bounds__(T) k_bs7_lanes(const int32_t *__restrict__ ids
 }
 
 int bs7_split_launch(const int32_t *ids, int64_t nl, const double *qg, int32_t split, const double *qh,
-                     double *ql, int has_mask, cudaStream_t st) {
+                     const double *qh1, const unsigned long long *cnt, double *ql, int has_mask, cudaStream_t st) {
     constexpr int T = 128, U = 4;
     const unsigned grid = (unsigned)std::max<int64_t>(1, (nl + T * U - 1) / (T * U));
     if (has_mask)
-        k_bs7_lanes<T, U, true, true><<<grid, T, 0, st>>>(ids, nl, qg, ql, split, qh);
+        k_bs7_lanes<T, U, true, true><<<grid, T, 0, st>>>(ids, nl, qg, ql, split, qh, qh1, cnt);
     else
-        k_bs7_lanes<T, U, false, true><<<grid, T, 0, st>>>(ids, nl, qg, ql, split, qh);
+        k_bs7_lanes<T, U, false, true><<<grid, T, 0, st>>>(ids, nl, qg, ql, split, qh, qh1, cnt);
     return launch_check("sb_bs7_scatter_split");
+}
+
+// BS7 halo put: n doubles of src into dst0 or dst1 by the parity of the call
+// count *cnt (read before the LSA barrier advances it; dist.py DistScatter)
+__global__ void k_halo_put(const double *__restrict__ src, double *dst0, double *dst1, int64_t n,
+                           const unsigned long long *__restrict__ cnt) {
+    double *dst = (*cnt & 1) ? dst1 : dst0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = ld_stream(src + i);
+}
+
+int halo_put_launch(const double *src, double *dst0, double *dst1, int64_t n, const unsigned long long *cnt,
+                    cudaStream_t st) {
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8));
+    k_halo_put<<<(unsigned)grid, 256, 0, st>>>(src, dst0, dst1, n, cnt);
+    return launch_check("sb_bs7_halo_put");
 }
 
 int bs7_lanes_launch(const int32_t *ids, int64_t nl, const double *qg, double *ql, int has_mask,

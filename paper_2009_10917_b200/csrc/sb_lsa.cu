@@ -80,9 +80,13 @@ namespace sb {
 __global__ void k_lsa_peer_ptr(ncclWindow_t w, size_t off, int peer, void **out) {
     *out = ncclGetLsaPointer(w, off, peer);
 }
-__global__ void k_lsa_barrier(ncclDevComm dc) {
+// (cnt: a call counter in this rank's memory, advanced after the barrier --
+// the BS7 halo buffers' parity, read by the put before and the split scatter
+// after it, dist.py DistScatter)
+__global__ void k_lsa_barrier(ncclDevComm dc, unsigned long long *cnt) {
     ncclLsaBarrierSession<ncclCoopThread> bar(ncclCoopThread(), dc, ncclTeamTagLsa(), 0);
     bar.sync(ncclCoopThread(), cuda::memory_order_acq_rel);
+    if (cnt) *cnt += 1;
 }
 }  // namespace sb
 
@@ -263,8 +267,18 @@ int sb_lsa_barrier(sb_lsa_t *ctx, sb_stream_t s) {
         set_error("sb_lsa_barrier: null context");
         return SB_E_INVALID;
     }
-    k_lsa_barrier<<<1, 1, 0, as_stream(s)>>>(ctx->dc);
+    k_lsa_barrier<<<1, 1, 0, as_stream(s)>>>(ctx->dc, nullptr);
     return launch_check("sb_lsa_barrier");
+}
+
+int sb_lsa_barrier_advance(sb_lsa_t *ctx, unsigned long long *call_count, sb_stream_t s) {
+    clear_error();
+    if (!ctx || !call_count) {
+        set_error("sb_lsa_barrier_advance: null argument");
+        return SB_E_INVALID;
+    }
+    k_lsa_barrier<<<1, 1, 0, as_stream(s)>>>(ctx->dc, call_count);
+    return launch_check("sb_lsa_barrier_advance");
 }
 
 int sb_lsa_cg_pap(const double *p, const double *ap, int64_t n, int64_t bs, int64_t nb, void *ws, sb_cg_state *st,

@@ -321,13 +321,17 @@ class DistScatter:
         self.exchange()
         self.scatter_fn(self.ids, self.window, q_local)
 
-    def enable_lsa(self, lsa, offset: int) -> None:
+    def enable_lsa(self, lsa, offset: int, counter_offset: int) -> None:
         """One-plane halo over NVLink: rank r+1 writes its bottom plane into
         rank r's halo buffer (2 planes at byte `offset` of the LSA halo window,
         alternating per call), one LSA barrier, then a split scatter reads the
-        own rows from `window` and the halo plane from the LSA buffer."""
+        own rows from `window` and the halo plane from the LSA buffer.  The
+        buffer parity is a call counter in this rank's window (8 bytes at
+        `counter_offset`) that the barrier kernel advances -- device state, so
+        captured CUDA graphs alternate correctly on every replay."""
         nb = 8 * self.part.plane
-        self.lsa, self.epoch = lsa, 0
+        self.lsa = lsa
+        self.counter = lsa.halo_pointers(counter_offset, self.rank)[0]
         self.halo_ptrs = ([lsa.halo_pointers(offset + e * nb, self.rank)[0] for e in (0, 1)]
                           if self.rank < self.part.world - 1 else None)
         self.down_ptrs = ([lsa.halo_pointers(offset + e * nb, self.rank - 1)[1] for e in (0, 1)]
@@ -337,23 +341,22 @@ class DistScatter:
         """BS7 over the slab with the NVLink halo; `own` (default: the window's
         own rows) holds this rank's q_global rows."""
         L = _lib.lib()
-        e = self.epoch
-        self.epoch ^= 1
         st = _lib.stream_handle(self.device)
         plane = self.part.plane
         src = self.window if own is None else own
-        if self.down_ptrs is not None:  # my bottom plane -> rank-1's halo buffer, over NVLink
-            _lib.check(L.sb_bs1_copy(src.data_ptr(), self.down_ptrs[e], plane, st), "bs7 halo put")
-        self.lsa.barrier()
+        if self.down_ptrs is not None:  # my bottom plane -> rank-1's halo buffer (call parity), over NVLink
+            _lib.check(L.sb_bs7_halo_put(src.data_ptr(), self.down_ptrs[0], self.down_ptrs[1], plane,
+                                         self.counter, st), "bs7 halo put")
+        self.lsa.barrier_advance(self.counter)
         nl = int(self.ids.shape[0])
         if self.halo_ptrs is None:  # last rank owns its top plane
             n_own = int(src.shape[0]) if own is not None else int(self.window.shape[0])
             _lib.check(L.sb_bs7_scatter(self.ids.data_ptr(), nl, src.data_ptr(), n_own, q_local.data_ptr(), 0, st),
                        "bs7_scatter")
         else:
-            _lib.check(L.sb_bs7_scatter_split(self.ids.data_ptr(), nl, src.data_ptr(), self.own_rows,
-                                              self.halo_ptrs[e], plane, q_local.data_ptr(), 0, st),
-                       "bs7_scatter_split")
+            _lib.check(L.sb_bs7_scatter_split_pair(self.ids.data_ptr(), nl, src.data_ptr(), self.own_rows,
+                                                   self.halo_ptrs[0], self.halo_ptrs[1], plane, self.counter,
+                                                   q_local.data_ptr(), 0, st), "bs7_scatter_split_pair")
 
 
 class DistMassOperator:
@@ -371,9 +374,9 @@ class DistMassOperator:
         self.scat = DistScatter.build(part, rank, device)
         self.gath = DistGather.build(part, rank, device)
         nb = 8 * part.plane
-        lsa.halo_window(4 * nb + 64)  # [BS6 carry x2 | BS7 halo x2 | BS6 sync words]
+        lsa.halo_window(4 * nb + 64)  # [BS6 carry x2 | BS7 halo x2 | BS6 sync words, BS7 call count]
         self.gath.enable_lsa(lsa, 0, sync_offset=4 * nb)
-        self.scat.enable_lsa(lsa, 2 * nb)
+        self.scat.enable_lsa(lsa, 2 * nb, counter_offset=4 * nb + 40)
         self.w = torch.as_tensor(weights, dtype=torch.float64).to(self.device)
         if self.w.shape[0] != part.nl(rank):
             raise ValueError("weights must have one entry per element-local node of this rank's slab")
@@ -499,9 +502,9 @@ class BenchContext:
         self.scat = DistScatter.build(self.part, self.rank, device)
         if self.lsa is not None:
             nb = 8 * self.part.plane
-            self.lsa.halo_window(4 * nb + 64)  # [BS6 carry x2 | BS7 halo x2 | BS6 sync words]
+            self.lsa.halo_window(4 * nb + 64)  # [BS6 carry x2 | BS7 halo x2 | BS6 sync words, BS7 call count]
             self.gather.enable_lsa(self.lsa, 0, sync_offset=4 * nb)
-            self.scat.enable_lsa(self.lsa, 2 * nb)
+            self.scat.enable_lsa(self.lsa, 2 * nb, counter_offset=4 * nb + 40)
             self.collective += ("; BS6 + carry halo in one launch (partials stored over NVLink into the "
                                 "peer's window, flag handshake); BS7 halo plane written over NVLink + LSA barrier")
             self.launches_per_step = 7 + 2  # + BS7's halo put and LSA barrier (BS6 is one fused launch)

@@ -134,6 +134,12 @@ class LsaReducer:
         """Collective LSA barrier on the current stream (one-thread kernel)."""
         _lib.check(self.L.sb_lsa_barrier(self.handle, _lib.stream_handle(self.device)), "sb_lsa_barrier")
 
+    def barrier_advance(self, counter_ptr: int) -> None:
+        """The barrier, then +1 on the uint64 call counter at counter_ptr (this
+        rank's memory): the BS7 halo buffers' parity, kept on the device."""
+        _lib.check(self.L.sb_lsa_barrier_advance(self.handle, counter_ptr, _lib.stream_handle(self.device)),
+                   "sb_lsa_barrier_advance")
+
     # a private zeroed workspace per config (the kernels leave it zeroed)
     def _workspace(self, cfg: ReductionConfig) -> torch.Tensor:
         key = (cfg.block_size, cfg.n_blocks)

@@ -141,6 +141,108 @@ def test_bs7_halo_through_lsa_window_bitexact(lsa, K, p, world):
         assert torch.equal(ql, want[lo:hi]), r
 
 
+@pytest.mark.parametrize("K,p,world", [(6, 3, 3), (5, 1, 4)])
+def test_bs7_halo_buffer_parity_on_device_under_graph_replay(lsa, K, p, world):
+    """The BS7 halo's two buffers alternate on a call counter in device memory
+    (sb_bs7_halo_put / sb_lsa_barrier_advance / sb_bs7_scatter_split_pair):
+    emulated ranks on this GPU, one captured call replayed 5 times (an odd
+    count per replay, which a host-side parity would freeze) -- every replay
+    bitwise, the counters at the call count, and the buffer written last
+    alternating."""
+    import paper_2009_10917_b200 as sb
+    from paper_2009_10917_b200 import _lib
+    from paper_2009_10917_b200 import dist as D
+    from paper_2009_10917_b200.mesh import build_slab_l2g
+    part = D.SlabPartition(K, p, world)
+    mesh = sb.build_mesh(K, p)
+    if not hasattr(lsa, "_halo_ok"):
+        lsa.halo_window(2 * 8 * 4_000_000)
+        lsa._halo_ok = True
+    L = _lib.lib()
+    plane, nb = part.plane, 8 * part.plane
+    stride = 2 * nb + 64
+    base = 8 * 1_000_000  # clear of the other tests' halo buffers
+
+    ptr = {}  # (halo_pointers is not capturable: resolve every address up front)
+    for r in range(world):
+        for off in (r * stride, r * stride + nb, r * stride + 2 * nb):
+            ptr[off] = lsa.halo_pointers(base + off, 0)
+
+    def loc(off):
+        return ptr[off][0]
+
+    def rem(off):
+        return ptr[off][1]
+
+    counters = [loc(r * stride + 2 * nb) for r in range(world)]
+    for r in range(world):  # fresh counters (the window is shared with other tests)
+        torch.cuda.synchronize()
+        _lib.check(L.sb_bs1_copy(torch.zeros(1, dtype=torch.float64, device="cuda").data_ptr(), counters[r], 1,
+                                 _lib.stream_handle()), "zero")
+    qg = torch.empty(mesh.ng, dtype=torch.float64, device="cuda")
+    ids, ql, own = [], [], []
+    for r in range(world):
+        z0, z1 = part.layers(r)
+        lo, hi = part.local_span(r)
+        a, b = part.read_span(r)
+        ids.append(build_slab_l2g(K, p, z0, z1) - a)
+        ql.append(torch.zeros(hi - lo, dtype=torch.float64, device="cuda"))
+        own.append(torch.empty(part.ng_own(r) if r < world - 1 else b - a, dtype=torch.float64, device="cuda"))
+
+    def call():
+        st = _lib.stream_handle()
+        for r in range(world):  # rank r's bottom plane -> rank r-1's halo buffer (rank r's parity)
+            a, _ = part.read_span(r)
+            own[r].copy_(qg[a:a + own[r].shape[0]])
+            if r > 0:
+                b0 = (r - 1) * stride
+                _lib.check(L.sb_bs7_halo_put(own[r].data_ptr(), rem(b0), rem(b0 + nb), plane, counters[r], st),
+                           "put")
+        for r in range(world):
+            lsa.barrier_advance(counters[r])
+        for r in range(world):
+            n = ids[r].shape[0]
+            if r < world - 1:
+                b0 = r * stride
+                _lib.check(L.sb_bs7_scatter_split_pair(ids[r].data_ptr(), n, own[r].data_ptr(), own[r].shape[0],
+                                                       loc(b0), loc(b0 + nb), plane, counters[r],
+                                                       ql[r].data_ptr(), 0, st), "split pair")
+            else:
+                _lib.check(L.sb_bs7_scatter(ids[r].data_ptr(), n, own[r].data_ptr(), own[r].shape[0],
+                                            ql[r].data_ptr(), 0, st), "scatter")
+
+    gen = torch.Generator(device="cuda"); gen.manual_seed(K + p)
+    qg.uniform_(-1, 1, generator=gen)
+    call()  # eager call 0 (buffer 0)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        call()
+    torch.cuda.current_stream().wait_stream(side)
+    l2g = mesh.local_to_global_dev.long()
+    for rep in range(5):
+        qg.uniform_(-1, 1, generator=gen)
+        g.replay()
+        torch.cuda.synchronize()
+        want = qg[l2g]
+        for r in range(world):
+            lo, hi = part.local_span(r)
+            assert torch.equal(ql[r], want[lo:hi]), (rep, r)
+        calls = rep + 2  # the eager call, the capture run none: replays only
+        for r in range(world):
+            cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+            _lib.check(L.sb_bs1_copy(counters[r], cnt.data_ptr(), 1, _lib.stream_handle()), "read")
+            assert int(cnt.item()) == calls, (rep, r, int(cnt.item()))
+        # the buffer the last put wrote holds rank 1's bottom plane, the other one an older plane
+        a1, _ = part.read_span(1)
+        last = torch.empty(plane, dtype=torch.float64, device="cuda")
+        _lib.check(L.sb_bs1_copy(loc(((calls - 1) & 1) * nb), last.data_ptr(), plane, _lib.stream_handle()), "rd")
+        torch.cuda.synchronize()
+        assert torch.equal(last, qg[a1:a1 + plane]), rep
+
+
 @pytest.mark.parametrize("fused,graph", [(True, False), (False, False), (True, True)])
 def test_device_cg_with_fused_combine_one_rank(lsa, fused, graph):
     """cg_solve_device with the multi-GPU reductions (sb_lsa_cg_*) on a one-rank
@@ -180,6 +282,10 @@ def test_dist_mass_operator_and_cg_one_rank(lsa):
         b = torch.from_numpy(rng.uniform(-1, 1, mesh.ng)).cuda()
         want = cg.cg_solve_device(A1, b, torch.zeros_like(b), 1e-22, 500, relative=True)
         got = cg.cg_solve_device(Ad, b, torch.zeros_like(b), 1e-22, 500, relative=True, lsa=ctx, check_every=8)
+        assert got.iterations == want.iterations and torch.equal(got.x, want.x)
+        # captured iterations, an odd number per replay (every halo parity is device-side)
+        got = cg.cg_solve_device(Ad, b, torch.zeros_like(b), 1e-22, 500, relative=True, lsa=ctx, check_every=7,
+                                 graph=True)
         assert got.iterations == want.iterations and torch.equal(got.x, want.x)
     finally:
         ctx.close()
