@@ -64,6 +64,9 @@ def parse_args(argv=None):
                     help="skip the worst-case configs (C3 N=1/2, BS1-BS5 at 1e9) and the T0/Wmax fit")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--strong", action="store_true",
+                    help="N>1: strong scaling -- --dofs is the global vector length (split across the "
+                         "ranks) and --mesh-k the global mesh (C4: --dofs 1e9; C5: --mesh-k 143)")
     ap.add_argument("--collective", choices=["nccl", "fused"], default="nccl",
                     help="N>1: NCCL collectives (default) or the fused in-kernel NVLink combine")
     ap.add_argument("--dry-run", action="store_true",
@@ -299,6 +302,10 @@ class Workload:
         self.dist = dist_ctx
         self.cfg = sb.ReductionConfig(args.block_size, args.n_blocks)
         n = int(args.n)
+        if dist_ctx is not None and args.strong:  # this rank's contiguous chunk of the global vector
+            from paper_2009_10917_b200.parallel import split_range
+            lo, hi = split_range(n, dist_ctx.world)[dist_ctx.rank]
+            n = hi - lo
         self.n = n
         gen = torch.Generator(device=device)
         gen.manual_seed(20091091 + (dist_ctx.rank if dist_ctx else 0))
@@ -622,8 +629,8 @@ def main_ours(args):
     if world > 1:
         # every rank's timings (device events on its own launch stream); the
         # step time is the max over ranks
-        mine = torch.tensor([step_ms] + [per_ms[k] for k in TESTS] + [iso_ms[k] for k in TESTS],
-                            dtype=torch.float64, device=device)
+        mine = torch.tensor([step_ms] + [per_ms[k] for k in TESTS] + [iso_ms[k] for k in TESTS]
+                            + [float(w.bytes[k]) for k in TESTS], dtype=torch.float64, device=device)
         if backend == "nccl":
             allr = torch.empty(world, mine.numel(), dtype=torch.float64, device=device)
             dist.all_gather_into_tensor(allr, mine)
@@ -632,23 +639,28 @@ def main_ours(args):
             parts = [torch.empty(mine.numel(), dtype=torch.float64) for _ in range(world)]
             dist.all_gather(parts, mine.cpu())
             allr = torch.stack(parts)
-        t = allr.max(dim=0).values
+        nt = len(TESTS)
+        t = allr[:, :2 * nt + 1].max(dim=0).values
         step_ms = float(t[0])
         per_ms = {k: float(t[i + 1]) for i, k in enumerate(TESTS)}
-        iso_ms = {k: float(t[len(TESTS) + i + 1]) for i, k in enumerate(TESTS)}
-        rank_bytes = sum(w.bytes.values())
+        iso_ms = {k: float(t[nt + i + 1]) for i, k in enumerate(TESTS)}
+        # bytes: every rank's own (slabs and vector chunks may differ by a layer / an element)
+        rank_bytes = allr[:, 2 * nt + 1:]
+        tot_bytes = {k: int(rank_bytes[:, i].sum()) for i, k in enumerate(TESTS)}
         per_rank = [{"rank": r, "ms_per_step": round(float(allr[r, 0]), 4),
-                     "GBps": round(rank_bytes / (float(allr[r, 0]) * 1e-3) / 1e9, 1),
+                     "GBps": round(float(rank_bytes[r].sum()) / (float(allr[r, 0]) * 1e-3) / 1e9, 1),
                      "device": f"cuda:{r % max(1, torch.cuda.device_count())}"}
                     for r in range(world)]
-    bytes_step = sum(w.bytes.values()) * world
+    else:
+        tot_bytes = dict(w.bytes)
+    bytes_step = sum(tot_bytes.values())
     value = bytes_step / (step_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
     agg_peak = peak * world
     per_test = {}
     for k in TESTS:
-        gbs = w.bytes[k] * world / (per_ms[k] * 1e-3) / 1e9
-        iso = w.bytes[k] * world / (iso_ms[k] * 1e-3) / 1e9
+        gbs = tot_bytes[k] / (per_ms[k] * 1e-3) / 1e9
+        iso = tot_bytes[k] / (iso_ms[k] * 1e-3) / 1e9
         per_test[k] = {"GBps": round(gbs, 1), "frac_of_peak": round(gbs / agg_peak, 4),
                        "ms": round(per_ms[k], 4), "bytes_per_rank": w.bytes[k],
                        "GBps_isolated": round(iso, 1), "frac_isolated": round(iso / agg_peak, 4)}
@@ -669,11 +681,15 @@ def main_ours(args):
         result = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if (args.strong and world > 1) else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: U(-1,1) fp64 drawn on device (seeded torch generator)",
-            "config": {"workload": f"BS1-BS5 at n={int(args.n):.0e} DOFs/GPU + BS6/BS7 on the "
-                                   f"K={args.K}, N={args.order} hex mesh (per GPU)",
-                       "n_per_gpu": int(args.n), "mesh": w.mesh_desc,
+            "config": {"workload": (f"BS1-BS5 at n={int(args.n):.0e} DOFs in total + BS6/BS7 on the global "
+                                    f"K={args.K}, N={args.order} hex mesh, split over {world} GPUs"
+                                    if (args.strong and world > 1) else
+                                    f"BS1-BS5 at n={int(args.n):.0e} DOFs/GPU + BS6/BS7 on the "
+                                    f"K={args.K}, N={args.order} hex mesh (per GPU)"),
+                       "n_per_gpu": w.n, "mesh": w.mesh_desc,
                        "reduction": [args.block_size, args.n_blocks],
                        "parallelism": f"slab{world}" if world > 1 else "single",
                        **({"collective": dist_ctx.collective} if dist_ctx is not None else {}),

@@ -440,8 +440,16 @@ def _create_with_deadline(make, seconds: float, expected_exc):
     return box.get("obj"), box.get("why")
 
 
+def global_mesh_k(K: int, world: int, strong: bool) -> int:
+    """bench.py's global mesh: weak scaling keeps the work per rank (K_g ~ K *
+    world^(1/3)); strong scaling (--strong) splits the K^3 mesh itself in
+    slabs (config 5: K = 143 on 8 GPUs).  At least one element layer per rank."""
+    return max(world, K if strong else int(round(K * world ** (1.0 / 3.0))))
+
+
 class BenchContext:
-    """Per-rank state of bench.py's weak-scaling step (n per rank, K_g^3 mesh)."""
+    """Per-rank state of bench.py's multi-GPU step (weak scaling: n per rank, a
+    K_g^3 mesh with K_g ~ K world^(1/3); --strong: n and K global)."""
 
     def __init__(self, rank: int, world: int, args, device, use_lsa: bool | None = None):
         import os
@@ -485,7 +493,7 @@ class BenchContext:
                     self.lsa.abort()  # local: some peer never built its context
                     self.lsa = None
                 self.collective += f" (fused path unavailable: {why or 'not on every rank'})"
-        Kg = max(world, int(round(args.K * world ** (1.0 / 3.0))))
+        Kg = global_mesh_k(args.K, world, getattr(args, "strong", False))
         self.part = SlabPartition(Kg, args.order, world)
         g = self.part.g
         self.mesh_desc = {"K_global": Kg, "order": args.order, "ng_global": g ** 3,

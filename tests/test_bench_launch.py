@@ -63,3 +63,19 @@ def test_setup_deadline_gives_up():
         raise RuntimeError("NCCL < 2.28")
     assert _create_with_deadline(refuse, 5, RuntimeError) == (None, "NCCL < 2.28")
     assert _create_with_deadline(lambda: 7, 5, RuntimeError) == (7, None)
+
+
+def test_strong_scaling_sizes():
+    """--strong: the global vector is split in rank chunks and the global mesh
+    in slabs (C4: n = 1e9 on 8 GPUs; C5: K = 143, 18 x 7 + 17 layers)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2009_10917_b200.dist import SlabPartition, global_mesh_k
+    from paper_2009_10917_b200.parallel import split_range
+    a = bench.parse_args(["--gpus", "8", "--strong", "--dofs", "1e9", "--mesh-k", "143"])
+    assert a.strong and int(a.n) == 10 ** 9 and a.K == 143
+    assert global_mesh_k(143, 8, True) == 143 and global_mesh_k(66, 8, False) == 132
+    assert [hi - lo for lo, hi in split_range(int(a.n), 8)] == [125_000_000] * 8
+    part = SlabPartition(143, 7, 8)
+    assert [z1 - z0 for z0, z1 in (part.layers(r) for r in range(8))] == [18] * 7 + [17]
+    assert not bench.parse_args([]).strong
